@@ -1,0 +1,433 @@
+"""Benchmark: fused SpMM-recurrence throughput on BASELINE config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
+SBM n=1e6 in 100 blocks, expected degree 15 intra + 5 inter, normalized
+adjacency (T ~ 2e7 stored nnz), d=80, L=180, f(x)=1{x>=0.95}, Philox
+projection generated on the device, row-normalised output.  One "step" = one
+whole embedding: projection init + 180 fused K1 steps + row normalisation.
+Headline dtype is f64 (the reference's arithmetic, bit-exact); an "fp32"
+object reports the same workload in fp32.
+
+value  = T*d*L / device time per step (CUDA events, inputs resident in HBM;
+         the working set -- 2 x 640 MB Q buffers + 640 MB E + 240 MB CSR in
+         f64 -- is far larger than the 126 MB L2, so no flush is needed).
+e2e    = same metric through the reference-facing C ABI call with HOST
+         buffers: CSR upload + projection block H2D + E D2H every step.
+roofline: K1's algorithmic bytes per launch, B = T*(4+8) + 5*n*d*8 (f64) /
+         T*(4+4) + 5*n*d*4 (f32), over K1's average launch time (CUDA events
+         on the library stream), against MEASURED_PEAKS.json hbm_gbs.
+N>1 (torchrun): columns are sharded across ranks (the matrix is replicated),
+one NCCL all-gather assembles E; value = total units / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused SpMM-recurrence nnz*d*L/s (config 2)"
+UNIT = "nnz*d*L/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, p in rows for i, v in enumerate(p[1:5]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(dtype: str):
+    """Per-launch dram bytes of K1 from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            return json.load(fh).get(dtype)
+    except (OSError, ValueError):
+        return None
+
+
+def k1_bytes(nnz: int, n: int, d: int, ld: int, dtype: str) -> int:
+    """north_star model: T*(idx+val) + 5*n*d*dtype (Y_l, Y_{l-1}, E read; Y_{l+1}, E written)."""
+    es = 8 if dtype == "f64" else 4
+    return nnz * (4 + es) + 5 * n * d * es
+
+
+def make_workload(n: int, seed: int = 2):
+    from paper_1509_08360_b200 import graphs
+
+    t0 = time.perf_counter()
+    S = graphs.sbm(n, 100, 15.0, 5.0, seed=seed)
+    log(f"[bench] SBM n={n} nnz={S.nnz} built in {time.perf_counter() - t0:.1f}s (host, untimed)")
+    return S
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_08360_b200 as pb
+    from paper_1509_08360_b200 import _lib
+    from paper_1509_08360_b200.distributed import column_shards
+
+    torch.cuda.set_device(local_rank)
+    S = make_workload(args.n)
+    f = pb.indicator_above(0.95)
+    coeffs = pb.legendre_coefficients(f, args.L).coeffs
+    n, nnz, d, L = S.n_rows, S.nnz, args.d, args.L
+    units = nnz * d * L
+    peak, peak_src = measured_peak()
+
+    def measure(dtype: str):
+        W = 2 if dtype == "f64" else 4
+        lo, hi = column_shards(d, world, W)[rank]
+        dm = pb.DeviceMatrix(S, "float64" if dtype == "f64" else "float32", local_rank)
+        plan = dm.plan(hi - lo)
+        ext = torch.cuda.ExternalStream(dm.ctx.stream, device=local_rank)
+        gather_buf = None
+
+        def one_step():
+            plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7, col0=lo, d_global=d,
+                     normalize_rows=(world == 1))
+            if world > 1:
+                nonlocal gather_buf
+                gather_buf = _gather_columns(plan, dm, n, d, world, rank, local_rank, dtype)
+
+        for _ in range(args.warmup):
+            one_step()
+        dm.ctx.sync()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k1_ms = []
+        with ClockSampler(local_rank) as clk:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(ext)
+            for _ in range(args.steps):
+                one_step()
+                if world == 1:
+                    pass
+            ev1.record(ext)
+            dm.ctx.sync()
+            torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / args.steps
+        # per-launch K1 time of the last step (events bracket the K1 launches only)
+        _, steps_ms, launches = plan.timing()
+        k1_ms = steps_ms / max(launches, 1)
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{local_rank}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        launches_per_step = launches + 1 + (1 if world == 1 else 0)
+        B = k1_bytes(nnz, n, hi - lo, plan.d, dtype)
+        achieved = B / (k1_ms * 1e-3) / 1e9
+        out = {
+            "value": units / (ms * 1e-3), "ms_per_step": ms, "k1_ms": k1_ms,
+            "gpu_launches_per_step": launches_per_step,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dtype),
+                         "algorithmic_bytes_per_launch": B, "peak_source": peak_src},
+            "clocks": clk.summary(),
+        }
+        return out, dm, plan
+
+    res64, dm64, plan64 = measure("f64")
+    log(f"[bench] f64: {res64['ms_per_step']:.2f} ms/step, K1 {res64['k1_ms']:.3f} ms, "
+        f"{res64['roofline']['achieved']:.0f} GB/s ({res64['roofline']['frac']:.3f})")
+    res32 = None
+    if not args.skip_fp32:
+        dm64.close()
+        res32, dm32, _ = measure("f32")
+        dm32.close()
+        log(f"[bench] f32: {res32['ms_per_step']:.2f} ms/step, K1 {res32['k1_ms']:.3f} ms, "
+            f"{res32['roofline']['achieved']:.0f} GB/s ({res32['roofline']['frac']:.3f})")
+
+    e2e = None
+    if not args.skip_e2e and world == 1:
+        e2e = run_e2e(args, S, coeffs, units, local_rank)
+        log(f"[bench] e2e: {e2e['ms_per_step']:.1f} ms/step -> {e2e['value']:.3e} {UNIT}")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu = cpu_baseline(S, d, coeffs, args.cpu_seconds)
+        log(f"[bench] cpu baseline: {cpu['value']:.3e} {UNIT} on {cpu['cores']} threads ({cpu['sample']})")
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res64["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res64["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded O(T) SBM sampler; Philox projection on device)",
+            "config": {"workload": "config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, "
+                                   "f=1{x>=0.95}, row-normalised",
+                       "n": n, "nnz": nnz, "d": d, "L": L,
+                       "parallelism": f"column-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+            "roofline": res64["roofline"], "clocks": res64["clocks"],
+            "gpu_launches": res64["gpu_launches_per_step"] * args.steps,
+            "e2e": None if e2e is None else {k: e2e[k] for k in ("value", "unit", "h2d_bytes_per_step",
+                                                                 "d2h_bytes_per_step")},
+            "cpu_baseline": cpu,
+            "k1_ms": res64["k1_ms"],
+        }
+        if res32 is not None:
+            line["fp32"] = {"value": res32["value"], "ms_per_step": res32["ms_per_step"], "k1_ms": res32["k1_ms"],
+                            "roofline": res32["roofline"], "clocks": res32["clocks"]}
+        print(json.dumps(line), flush=True)
+
+
+def _gather_columns(plan, dm, n, d, world, rank, local_rank, dtype):
+    """All-gather each rank's E column slice (NCCL) and row-normalise the assembled E."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_08360_b200.distributed import assemble_columns
+
+    from paper_1509_08360_b200 import _lib
+
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    local = torch.empty((n, plan.d), dtype=tdt, device=f"cuda:{local_rank}")
+    plan.copy_output_to(local.data_ptr(), plan.d)
+    dm.ctx.sync()
+    E = assemble_columns(local, world, d, dtype)
+    torch.cuda.current_stream().synchronize()
+    _lib.check(dm.lib.csemb_rownorm(dm.ctx.handle, E.data_ptr(), n, d, d, _lib.F64 if dtype == "f64" else _lib.F32))
+    return E
+
+
+def run_e2e(args, S, coeffs, units, device):
+    """Reference-facing call with host buffers: upload CSR + block, run, download E."""
+    import torch
+
+    import paper_1509_08360_b200 as pb
+    from paper_1509_08360_b200 import _lib
+
+    n, d = S.n_rows, args.d
+    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    ro, ci, va = pin(S.row_offsets), pin(S.col_indices), pin(S.values)
+    block = pin(pb.sample_projection(n, d, 7))
+    out = torch.empty((n, d), dtype=torch.float64).pin_memory()
+    ctx = _lib.context(device)
+    lib = ctx.lib
+    import ctypes as C
+
+    h2d = ro.numel() * 8 + ci.numel() * 8 + va.numel() * 8 + block.numel() * 8
+    d2h = out.numel() * 8
+    c = np.ascontiguousarray(coeffs)
+
+    def step():
+        h = C.c_void_p()
+        _lib.check(lib.csemb_matrix_upload(ctx.handle, n, n, S.nnz, C.c_void_p(ro.data_ptr()),
+                                           C.c_void_p(ci.data_ptr()), C.c_void_p(va.data_ptr()), _lib.F64,
+                                           C.byref(h)))
+        dm = pb.DeviceMatrix(None, "float64", device, _handle=h)
+        p = dm.plan(d)
+        rc = lib.csemb_apply_expansion(p.handle, _lib.ptr(c), len(c) - 1, 1, C.c_void_p(block.data_ptr()),
+                                       _lib.OMEGA_GIVEN, 0, 0, d, 1, C.c_void_p(out.data_ptr()), None, None, None)
+        _lib.check(rc)
+        dm.close()
+
+    for _ in range(2):
+        step()
+    times = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.median(times)
+    return {"value": units / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (the oracle port of the reference's algorithm)
+# ---------------------------------------------------------------------------
+def _cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(S, d, coeffs, seconds: float):
+    import oracle as O
+
+    cores = _cpu_cores()
+    O.set_threads(cores)
+    csr = O.CSR.of(S)
+    om = O.sample_projection(S.n_rows, d, 7)
+    t0 = time.perf_counter()
+    O.run_stage(csr, coeffs[:2], om)
+    t1 = time.perf_counter() - t0
+    order = int(max(1, min(len(coeffs) - 1, round(seconds / max(t1, 1e-3)))))
+    t0 = time.perf_counter()
+    O.run_stage(csr, coeffs[: order + 1], om)
+    t = time.perf_counter() - t0
+    return {"value": S.nnz * d * order / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{order} of {len(coeffs) - 1} recurrence steps of config 2 (n={S.n_rows}, d={d}, f64), "
+                      f"oracle/csemb_oracle.c restating engine._run_stage + scipy csr_matvecs, OpenMP over rows",
+            "seconds": t}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import oracle as O
+
+    import paper_1509_08360_b200 as pb
+
+    S = make_workload(args.n)
+    d = args.d
+    coeffs = pb.legendre_coefficients(pb.indicator_above(0.95), args.L).coeffs
+    cores = _cpu_cores()
+    O.set_threads(cores)
+    csr = O.CSR.of(S)
+    om = O.sample_projection(S.n_rows, d, 7)
+    t0 = time.perf_counter()
+    O.run_stage(csr, coeffs[:2], om)
+    t1 = time.perf_counter() - t0
+    order = int(max(1, min(args.L, round(args.ref_step_seconds / max(t1, 1e-3)))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.run_stage(csr, coeffs[: order + 1], om)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    v = S.nnz * d * order / sec
+    sample = (f"{order} of {args.L} recurrence steps per step of config 2 (n={S.n_rows}, nnz={S.nnz}, d={d}, f64); "
+              "oracle/csemb_oracle.c (restatement of engine._run_stage + scipy csr_matvecs), OpenMP over rows")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded O(T) SBM sampler)",
+        "config": {"workload": "config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, f=1{x>=0.95}",
+                   "n": S.n_rows, "nnz": S.nnz, "d": d, "L": args.L, "parallelism": "CPU threads"},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--d", type=int, default=80)
+    ap.add_argument("--L", type=int, default=180)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=6.0)
+    ap.add_argument("--skip-fp32", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rule)")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * csemb_cuda.h -- C ABI of the B200-native fused SpMM-Legendre recurrence
+ * (compressive spectral embedding, arXiv 1509.08360).
+ *
+ * Reference = the `csemb` Python package (/root/reference/pkg/src/csemb).
+ * It has no formal plugin API; its single seam for this path is
+ *   engine._apply_expansion(S, expansion, block, *, stage, n_workers, counter)
+ *   (engine.py:231-258), plus sample_projection (engine.py:79-99),
+ *   estimate_spectral_norm (engine.py:165-192) and scale_values (sparse.py:295-301).
+ * Each entry point below names the reference function it replaces.
+ *
+ * Conventions
+ *   - Every function returns an int status (CSEMB_OK = 0) and never throws;
+ *     csemb_last_error() returns a thread-local message for the last failure.
+ *   - Host pointers are borrowed for the duration of the call.
+ *   - Device buffers are owned by the opaque handles.
+ *   - Matrices are CSR with int64 row offsets / int64 column indices / f64
+ *     values on the host side, exactly the reference's SparseMatrix arrays
+ *     (sparse.py:55-99, design decision D6 64-bit indices).
+ *   - Dense blocks are n_rows x d, row-major, float64 on the host side.
+ *   - One context per device; calls on one context are serialised by a
+ *     mutex; all work of a context runs on that context's CUDA stream.
+ */
+#ifndef CSEMB_CUDA_H
+#define CSEMB_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSEMB_ABI_VERSION 1
+
+/* status codes */
+#define CSEMB_OK 0
+#define CSEMB_ERR_INVALID 1     /* bad argument: Python shim raises ValueError   */
+#define CSEMB_ERR_CUDA 2        /* CUDA runtime failure                          */
+#define CSEMB_ERR_NOMEM 3       /* device allocation failed                      */
+#define CSEMB_ERR_DIVERGED 4    /* non-finite iterate: DivergenceError            */
+#define CSEMB_ERR_UNSUPPORTED 5 /* valid request this build does not handle      */
+
+/* arithmetic types */
+#define CSEMB_F64 0
+#define CSEMB_F32 1
+
+/* projection-block sources */
+#define CSEMB_OMEGA_GIVEN 0    /* caller supplies the block                      */
+#define CSEMB_OMEGA_SPLITMIX 1 /* the reference's hash, bit-exact (engine.py:79) */
+#define CSEMB_OMEGA_PHILOX 2   /* Philox4x32-10 signs (benchmark generator)      */
+
+typedef struct csemb_ctx csemb_ctx;
+typedef struct csemb_mat csemb_mat;
+typedef struct csemb_plan csemb_plan;
+
+const char *csemb_last_error(void);
+int csemb_abi_version(void);
+int csemb_device_count(int *out);
+
+/* ---- context ------------------------------------------------------------ */
+int csemb_ctx_create(int device, csemb_ctx **out);
+int csemb_ctx_destroy(csemb_ctx *ctx);
+/* the context's cudaStream_t, for callers that time or order work on it */
+void *csemb_ctx_stream(csemb_ctx *ctx);
+int csemb_ctx_sync(csemb_ctx *ctx);
+int csemb_ctx_sm_count(csemb_ctx *ctx, int *out);
+
+/* ---- matrices -------------------------------------------------------------
+ * csemb_matrix_upload replaces SparseMatrix._csr (sparse.py:160-165): the CSR
+ * is validated for shape, copied once and kept device-resident (int64 row
+ * offsets, int32 column indices, values in `dtype`).  */
+int csemb_matrix_upload(csemb_ctx *ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                        const int64_t *row_offsets, const int64_t *col_indices,
+                        const double *values, int dtype, csemb_mat **out);
+/* same, from device pointers (int64 offsets, int64 or int32 indices
+ * per idx_bytes = 8|4, f64 values); used by device-side input builders */
+int csemb_matrix_upload_device(csemb_ctx *ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                               const void *row_offsets_dev, const void *col_indices_dev,
+                               int idx_bytes, const double *values_dev, int dtype,
+                               csemb_mat **out);
+int csemb_matrix_destroy(csemb_mat *m);
+int csemb_matrix_info(csemb_mat *m, int64_t *n_rows, int64_t *n_cols, int64_t *nnz, int *dtype);
+/* scale_values (sparse.py:295-301): values *= factor on the device (same
+ * IEEE product as numpy's S.values * factor). */
+int csemb_matrix_scale(csemb_mat *m, double factor);
+/* copy the device values back (f64) -- for tests of csemb_matrix_scale */
+int csemb_matrix_download_values(csemb_mat *m, double *values_out);
+
+/* ---- plans: device workspace for one (matrix, d) ----------------------------
+ * Holds Y (two n x ld buffers, Q(r-1) and Q(r-2)/Q(r) in place), E (n x ld)
+ * and the per-step diagnostics.  ld = d rounded up to 16 bytes.  */
+int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out);
+int csemb_plan_destroy(csemb_plan *p);
+
+/* Device-resident run: _apply_expansion (engine.py:231-258) chained over
+ * n_stages cascade stages (engine.py:332-336).  coeffs[0..order] are the
+ * stage's Legendre coefficients (LegendreExpansion.coeffs).  The projection
+ * block is `block_dev` (device, n x d f64 row-major) when omega_kind ==
+ * CSEMB_OMEGA_GIVEN, else generated on the device for global columns
+ * [col0, col0+d) of an n x d_global block with `seed`.  normalize_rows != 0
+ * appends the row normalisation (zero rows stay 0).  Asynchronous on the
+ * context stream; results stay in the plan.  */
+int csemb_plan_run(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                   const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
+                   int64_t d_global, int normalize_rows);
+/* Output access.  download converts to f64 (out_dtype CSEMB_F64) or f32. */
+int csemb_plan_download(csemb_plan *p, void *out_host, int out_dtype);
+int csemb_plan_output(csemb_plan *p, void **dev_ptr, int64_t *ld, int *dtype);
+/* Device-to-device copy of E (n x d, plan dtype) into dst with row stride
+ * dst_ld elements, on the context stream (for NCCL assembly of column shards). */
+int csemb_plan_copy_output(csemb_plan *p, void *dst_dev, int64_t dst_ld);
+/* Synchronises; max_abs (optional) receives n_stages*order*n_chunks values,
+ * n_chunks = ceil(d_global/32): the reference's per-32-column-chunk max|Q(r)|
+ * (engine.py:217-220).  first_bad_r / bad_stage follow the reference's
+ * DivergenceError (engine.py:221-225): 0 when every iterate is finite.  */
+int csemb_plan_diagnostics(csemb_plan *p, double *max_abs, int *first_bad_r, int *bad_stage);
+/* CUDA-event timings of the last run: whole run and the recurrence steps */
+int csemb_plan_timing(csemb_plan *p, float *ms_total, float *ms_steps, int *step_launches);
+
+/* Host-to-host drop-in for _apply_expansion (engine.py:231-258): uploads
+ * `block_host` (n x d f64; NULL when omega_kind generates it), runs, and
+ * writes `out_host` (n x d f64).  Returns CSEMB_ERR_DIVERGED with
+ * *first_bad_r / *bad_stage set if an iterate was non-finite.  */
+int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                          const double *block_host, int omega_kind, uint64_t seed,
+                          int64_t col0, int64_t d_global, int normalize_rows,
+                          double *out_host, double *max_abs, int *first_bad_r, int *bad_stage);
+
+/* ---- projection block: sample_projection (engine.py:79-99) -----------------
+ * Columns [col0, col0+w) of the n x d_global block, hashed with the global d.
+ * kind CSEMB_OMEGA_SPLITMIX is bit-identical to the reference.  */
+int csemb_sample_projection(csemb_ctx *ctx, int64_t n, int64_t d_global, uint64_t seed,
+                            int64_t col0, int64_t w, int kind, double *out_host);
+
+/* ---- row normalisation (K4) of an external device block -------------------
+ * E_i <- E_i / ||E_i||, zero rows stay 0 (the semantics of the reference's
+ * cosine harness, oracle.py:88-96); used after assembling column shards.  */
+int csemb_rownorm(csemb_ctx *ctx, void *E_dev, int64_t n, int64_t d, int64_t ld, int dtype);
+
+/* ---- spectral norm: estimate_spectral_norm (engine.py:165-192) -------------
+ * k start vectors: v0_host (n x k f64, unnormalised -- pass the reference's
+ * PCG64 block for parity) or NULL for Philox normals from `seed`.  Returns
+ * max over iterations of max|Rayleigh quotient| times `safety`.  */
+int csemb_spectral_norm(csemb_mat *m, int iters, int64_t k, const double *v0_host,
+                        uint64_t seed, double safety, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSEMB_CUDA_H */

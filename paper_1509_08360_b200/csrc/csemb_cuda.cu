@@ -1,0 +1,906 @@
+// csemb_cuda.cu -- C ABI (include/csemb_cuda.h) over the sm_100a kernels in kernels.cuh.
+//
+// Host-side runtime: contexts (device + stream + mutex), device-resident CSR
+// matrices, plans (Y/E workspaces + diagnostics), kernel dispatch.  No torch
+// types cross this boundary; the Python shim binds it with ctypes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/csemb_cuda.h"
+#include "kernels.cuh"
+
+using namespace csemb;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(...)                                                                            \
+    do {                                                                                   \
+        cudaError_t e_ = (__VA_ARGS__);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            cudaGetLastError();                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, \
+                        "%s failed: %s (%s:%d)", #__VA_ARGS__, cudaGetErrorString(e_), __FILE__,     \
+                        __LINE__);                                                         \
+        }                                                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct csemb_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+};
+
+struct csemb_mat {
+    csemb_ctx *ctx = nullptr;
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;
+    int dtype = CSEMB_F64;
+    int64_t *rowptr = nullptr;
+    int *cols = nullptr;
+    void *vals = nullptr;
+};
+
+struct csemb_plan {
+    csemb_mat *m = nullptr;
+    int64_t d = 0, ld = 0;  // ld in elements
+    void *y[2] = {nullptr, nullptr};
+    void *E = nullptr;
+    double *staging = nullptr;  // n x d f64 block staging (lazy)
+    size_t staging_bytes = 0;
+    unsigned long long *peaks = nullptr;
+    size_t peaks_cap = 0;  // elements
+    // last run
+    int order = 0, n_stages = 0;
+    int64_t n_chunks = 0;
+    int step_launches = 0;
+    bool ran = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+static size_t dsize(int dtype) { return dtype == CSEMB_F32 ? 4 : 8; }
+static int vec_w(int dtype) { return dtype == CSEMB_F32 ? 4 : 2; }
+
+static int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8) {
+    int64_t g = (work_items + threads - 1) / threads;
+    int64_t cap = (int64_t)sm_count * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// K1 dispatch: G lanes per row, VPL 16-byte vectors per lane
+// ---------------------------------------------------------------------------
+static std::mutex g_occ_mu;
+static std::unordered_map<const void *, int> g_occ;
+
+template <typename T, int G, int VPL, int MODE>
+static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
+    const void *fn = (const void *)k_step<T, G, VPL, MODE>;
+    const int threads = 256;
+    const int W = Vec<T>::W;
+    const int nch = ((P.col0 + (P.v0 + P.nvt) * W - 1) >> 5) - ((P.col0 + P.v0 * W) >> 5) + 1;
+    const size_t smem = MODE == MODE_RECUR ? (size_t)(nch + 1) * 8 : 0;
+    int per_sm;
+    {
+        std::lock_guard<std::mutex> lk(g_occ_mu);
+        auto it = g_occ.find(fn);
+        if (it == g_occ.end()) {
+            int nb = 0;
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, 1024);
+            if (e != cudaSuccess) return e;
+            it = g_occ.emplace(fn, std::max(1, nb)).first;
+        }
+        per_sm = it->second;
+    }
+    const int grid = grid_for(P.n_rows * G, threads, sm_count, per_sm);
+    k_step<T, G, VPL, MODE><<<grid, threads, smem, s>>>(P);
+    return cudaGetLastError();
+}
+
+template <typename T, int G, int MODE>
+static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, int sm) {
+    if (G == 1) {
+        switch (vpl) {
+            case 1: return run_step<T, G, 1, MODE>(P, s, sm);
+            case 2: return run_step<T, G, 2, MODE>(P, s, sm);
+            case 3: return run_step<T, G, 3, MODE>(P, s, sm);
+            default: break;
+        }
+    }
+    switch (vpl) {
+        case 4: return run_step<T, G, 4, MODE>(P, s, sm);
+        case 5: return run_step<T, G, 5, MODE>(P, s, sm);
+        case 6: return run_step<T, G, 6, MODE>(P, s, sm);
+        case 7: return run_step<T, G, 7, MODE>(P, s, sm);
+        case 8: return run_step<T, G, 8, MODE>(P, s, sm);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// G = largest power of two <= nv/4 (>= 1, <= 32), so VPL = ceil(nv/G) in [4, 8]
+// for nv >= 8 and = nv below; a launch covers at most 256 vectors.
+static int choose_group(int nv) {
+    int q = std::max(1, nv / 4);
+    int g = 1;
+    while (g * 2 <= q && g < 32) g *= 2;
+    return g;
+}
+
+static const int MAX_TILE_VECS = 256;
+
+template <typename T, int MODE>
+static cudaError_t launch_step(StepParams P, cudaStream_t s, int sm) {
+    const int nv_total = P.nvt;
+    const int ntiles = (nv_total + MAX_TILE_VECS - 1) / MAX_TILE_VECS;
+    const int base = P.v0;
+    for (int t = 0; t < ntiles; ++t) {
+        const int lo = (int)((int64_t)nv_total * t / ntiles), hi = (int)((int64_t)nv_total * (t + 1) / ntiles);
+        P.v0 = base + lo;
+        P.nvt = hi - lo;
+        const int G = choose_group(P.nvt);
+        const int vpl = (P.nvt + G - 1) / G;
+        cudaError_t e;
+        switch (G) {
+            case 1: e = dispatch_vpl<T, 1, MODE>(vpl, P, s, sm); break;
+            case 2: e = dispatch_vpl<T, 2, MODE>(vpl, P, s, sm); break;
+            case 4: e = dispatch_vpl<T, 4, MODE>(vpl, P, s, sm); break;
+            case 8: e = dispatch_vpl<T, 8, MODE>(vpl, P, s, sm); break;
+            case 16: e = dispatch_vpl<T, 16, MODE>(vpl, P, s, sm); break;
+            default: e = dispatch_vpl<T, 32, MODE>(vpl, P, s, sm); break;
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+static int tiles_for(int nv) { return (nv + MAX_TILE_VECS - 1) / MAX_TILE_VECS; }
+
+// ---------------------------------------------------------------------------
+// misc API
+// ---------------------------------------------------------------------------
+extern "C" const char *csemb_last_error(void) { return g_err.c_str(); }
+extern "C" int csemb_abi_version(void) { return CSEMB_ABI_VERSION; }
+
+extern "C" int csemb_device_count(int *out) {
+    if (!out) return fail(CSEMB_ERR_INVALID, "null out");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *out = 0;
+        return CSEMB_OK;
+    }
+    *out = n;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_ctx_create(int device, csemb_ctx **out) {
+    if (!out) return fail(CSEMB_ERR_INVALID, "null out");
+    *out = nullptr;
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n)
+        return fail(CSEMB_ERR_INVALID, "device %d out of range (have %d)", device, n);
+    CK(cudaSetDevice(device));
+    csemb_ctx *c = new csemb_ctx();
+    c->device = device;
+    cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(CSEMB_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_ctx_destroy(csemb_ctx *c) {
+    if (!c) return CSEMB_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return CSEMB_OK;
+}
+
+extern "C" void *csemb_ctx_stream(csemb_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+extern "C" int csemb_ctx_sync(csemb_ctx *c) {
+    if (!c) return fail(CSEMB_ERR_INVALID, "null context");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_ctx_sm_count(csemb_ctx *c, int *out) {
+    if (!c || !out) return fail(CSEMB_ERR_INVALID, "null argument");
+    *out = c->sm_count;
+    return CSEMB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// matrices
+// ---------------------------------------------------------------------------
+static void mat_free(csemb_mat *m) {
+    if (!m) return;
+    cudaFree(m->rowptr);
+    cudaFree(m->cols);
+    cudaFree(m->vals);
+    delete m;
+}
+
+static int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, int dtype,
+                     csemb_mat **out) {
+    if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(CSEMB_ERR_INVALID, "negative matrix dimension");
+    if (dtype != CSEMB_F64 && dtype != CSEMB_F32) return fail(CSEMB_ERR_INVALID, "dtype must be CSEMB_F64 or CSEMB_F32");
+    if (n_cols > 0x7FFFFFFFLL || n_rows > 0x7FFFFFFFLL)
+        return fail(CSEMB_ERR_UNSUPPORTED, "matrix dimension above 2^31-1 (int32 column indices)");
+    csemb_mat *m = new csemb_mat();
+    m->ctx = c;
+    m->n_rows = n_rows;
+    m->n_cols = n_cols;
+    m->nnz = nnz;
+    m->dtype = dtype;
+    cudaError_t e = cudaMalloc(&m->rowptr, sizeof(int64_t) * (size_t)(n_rows + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&m->cols, sizeof(int) * (size_t)std::max<int64_t>(nnz, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&m->vals, dsize(dtype) * (size_t)std::max<int64_t>(nnz, 1));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mat_free(m);
+        return fail(e == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA,
+                    "matrix allocation (%lld rows, %lld nnz): %s", (long long)n_rows,
+                    (long long)nnz, cudaGetErrorString(e));
+    }
+    *out = m;
+    return CSEMB_OK;
+}
+
+// convert staged f64 values / int64-or-int32 indices into the device CSR
+static int mat_fill_chunk(csemb_mat *m, int64_t off, int64_t cnt, const void *cols_dev, int idx_bytes,
+                          const double *vals_dev, int *bad_dev) {
+    cudaStream_t s = m->ctx->stream;
+    const int g = grid_for(cnt, 256, m->ctx->sm_count);
+    if (idx_bytes == 8)
+        k_cols_to_i32<<<g, 256, 0, s>>>((const int64_t *)cols_dev, m->cols + off, cnt, m->n_cols, bad_dev);
+    else
+        k_cols_check_i32<<<g, 256, 0, s>>>((const int *)cols_dev, m->cols + off, cnt, m->n_cols, bad_dev);
+    if (m->dtype == CSEMB_F64)
+        k_vals_convert<double><<<g, 256, 0, s>>>(vals_dev, (double *)m->vals + off, cnt);
+    else
+        k_vals_convert<float><<<g, 256, 0, s>>>(vals_dev, (float *)m->vals + off, cnt);
+    CK(cudaGetLastError());
+    return CSEMB_OK;
+}
+
+static int check_offsets_host(const int64_t *ro, int64_t n_rows, int64_t nnz) {
+    if (ro[0] != 0 || ro[n_rows] != nnz)
+        return fail(CSEMB_ERR_INVALID, "row_offsets must run from 0 to nnz");
+    for (int64_t i = 0; i < n_rows; ++i)
+        if (ro[i + 1] < ro[i]) return fail(CSEMB_ERR_INVALID, "row_offsets must be non-decreasing");
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                   const int64_t *row_offsets, const int64_t *col_indices,
+                                   const double *values, int dtype, csemb_mat **out) {
+    if (!c || !out || !row_offsets || (nnz > 0 && (!col_indices || !values)))
+        return fail(CSEMB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    *out = nullptr;
+    CK(cudaSetDevice(c->device));
+    if (n_rows < 0 || nnz < 0) return fail(CSEMB_ERR_INVALID, "negative matrix dimension");
+    int rc = check_offsets_host(row_offsets, n_rows, nnz);
+    if (rc) return rc;
+    csemb_mat *m = nullptr;
+    rc = mat_alloc(c, n_rows, n_cols, nnz, dtype, &m);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    cudaError_t e = cudaMemcpyAsync(m->rowptr, row_offsets, sizeof(int64_t) * (size_t)(n_rows + 1),
+                                    cudaMemcpyHostToDevice, s);
+    const int64_t CH = std::min<int64_t>(std::max<int64_t>(nnz, 1), (int64_t)1 << 25);
+    void *st_cols = nullptr, *st_vals = nullptr;
+    int *bad = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&st_cols, 8 * (size_t)CH);
+    if (e == cudaSuccess) e = cudaMalloc(&st_vals, 8 * (size_t)CH);
+    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+    for (int64_t off = 0; e == cudaSuccess && off < nnz; off += CH) {
+        const int64_t cnt = std::min(CH, nnz - off);
+        e = cudaMemcpyAsync(st_cols, col_indices + off, 8 * (size_t)cnt, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(st_vals, values + off, 8 * (size_t)cnt, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            rc = mat_fill_chunk(m, off, cnt, st_cols, 8, (const double *)st_vals, bad);
+            if (rc) break;
+        }
+        // the staging buffers are reused: finish this chunk before the next copy
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    int hbad = 0;
+    if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
+    cudaFree(st_cols);
+    cudaFree(st_vals);
+    cudaFree(bad);
+    if (rc || e != cudaSuccess) {
+        mat_free(m);
+        if (rc) return rc;
+        cudaGetLastError();
+        return fail(CSEMB_ERR_CUDA, "matrix upload: %s", cudaGetErrorString(e));
+    }
+    if (hbad) {
+        mat_free(m);
+        return fail(CSEMB_ERR_INVALID, "column index out of range");
+    }
+    *out = m;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_upload_device(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                          const void *row_offsets_dev, const void *col_indices_dev,
+                                          int idx_bytes, const double *values_dev, int dtype,
+                                          csemb_mat **out) {
+    if (!c || !out || !row_offsets_dev || (nnz > 0 && (!col_indices_dev || !values_dev)))
+        return fail(CSEMB_ERR_INVALID, "null argument");
+    if (idx_bytes != 4 && idx_bytes != 8) return fail(CSEMB_ERR_INVALID, "idx_bytes must be 4 or 8");
+    std::lock_guard<std::mutex> lk(c->mu);
+    *out = nullptr;
+    CK(cudaSetDevice(c->device));
+    csemb_mat *m = nullptr;
+    int rc = mat_alloc(c, n_rows, n_cols, nnz, dtype, &m);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    int *bad = nullptr;
+    cudaError_t e = cudaMemcpyAsync(m->rowptr, row_offsets_dev, sizeof(int64_t) * (size_t)(n_rows + 1),
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+    if (e == cudaSuccess && nnz > 0) rc = mat_fill_chunk(m, 0, nnz, col_indices_dev, idx_bytes, values_dev, bad);
+    int hbad = 0;
+    int64_t ends[2] = {0, 0};
+    if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&ends[0], m->rowptr, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&ends[1], m->rowptr + n_rows, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
+    cudaFree(bad);
+    if (rc || e != cudaSuccess) {
+        mat_free(m);
+        if (rc) return rc;
+        cudaGetLastError();
+        return fail(CSEMB_ERR_CUDA, "device matrix upload: %s", cudaGetErrorString(e));
+    }
+    if (hbad || ends[0] != 0 || ends[1] != nnz) {
+        mat_free(m);
+        return fail(CSEMB_ERR_INVALID, hbad ? "column index out of range" : "row_offsets must run from 0 to nnz");
+    }
+    *out = m;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_destroy(csemb_mat *m) {
+    if (!m) return CSEMB_OK;
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    mat_free(m);
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_info(csemb_mat *m, int64_t *n_rows, int64_t *n_cols, int64_t *nnz, int *dtype) {
+    if (!m) return fail(CSEMB_ERR_INVALID, "null matrix");
+    if (n_rows) *n_rows = m->n_rows;
+    if (n_cols) *n_cols = m->n_cols;
+    if (nnz) *nnz = m->nnz;
+    if (dtype) *dtype = m->dtype;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_scale(csemb_mat *m, double factor) {
+    if (!m) return fail(CSEMB_ERR_INVALID, "null matrix");
+    if (factor == 0.0 || !std::isfinite(factor))
+        return fail(CSEMB_ERR_INVALID, "scale factor must be finite and nonzero");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    CK(cudaSetDevice(m->ctx->device));
+    if (m->nnz == 0) return CSEMB_OK;
+    const int g = grid_for(m->nnz, 256, m->ctx->sm_count);
+    if (m->dtype == CSEMB_F64)
+        k_vals_scale<double><<<g, 256, 0, m->ctx->stream>>>((double *)m->vals, m->nnz, factor);
+    else
+        k_vals_scale<float><<<g, 256, 0, m->ctx->stream>>>((float *)m->vals, m->nnz, factor);
+    CK(cudaGetLastError());
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_matrix_download_values(csemb_mat *m, double *values_out) {
+    if (!m || (m->nnz && !values_out)) return fail(CSEMB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    CK(cudaSetDevice(m->ctx->device));
+    if (!m->nnz) return CSEMB_OK;
+    cudaStream_t s = m->ctx->stream;
+    if (m->dtype == CSEMB_F64) {
+        CK(cudaMemcpyAsync(values_out, m->vals, 8 * (size_t)m->nnz, cudaMemcpyDeviceToHost, s));
+    } else {
+        double *tmp = nullptr;
+        CK(cudaMalloc(&tmp, 8 * (size_t)m->nnz));
+        k_vals_to_f64<float><<<grid_for(m->nnz, 256, m->ctx->sm_count), 256, 0, s>>>((const float *)m->vals, tmp, m->nnz);
+        cudaError_t e = cudaMemcpyAsync(values_out, tmp, 8 * (size_t)m->nnz, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(tmp);
+        CK(e);
+    }
+    CK(cudaStreamSynchronize(s));
+    return CSEMB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+static void plan_free(csemb_plan *p) {
+    if (!p) return;
+    cudaFree(p->y[0]);
+    cudaFree(p->y[1]);
+    cudaFree(p->E);
+    cudaFree(p->staging);
+    cudaFree(p->peaks);
+    for (auto &e : p->ev)
+        if (e) cudaEventDestroy(e);
+    delete p;
+}
+
+extern "C" int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out) {
+    if (!m || !out) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (d < 1) return fail(CSEMB_ERR_INVALID, "d must be >= 1");
+    if (m->n_rows != m->n_cols) return fail(CSEMB_ERR_INVALID, "the recurrence needs a square (symmetric) matrix");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    *out = nullptr;
+    CK(cudaSetDevice(m->ctx->device));
+    csemb_plan *p = new csemb_plan();
+    p->m = m;
+    p->d = d;
+    const int W = vec_w(m->dtype);
+    p->ld = (d + W - 1) / W * W;
+    if (p->ld / W > 0x7FFFFFFF) {
+        delete p;
+        return fail(CSEMB_ERR_UNSUPPORTED, "d too large");
+    }
+    const size_t bytes = dsize(m->dtype) * (size_t)std::max<int64_t>(m->n_rows, 1) * (size_t)p->ld;
+    cudaError_t e = cudaMalloc(&p->y[0], bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->y[1], bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&p->E, bytes);
+    for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&p->ev[i]);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        plan_free(p);
+        return fail(e == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA,
+                    "plan allocation (3 x %zu bytes): %s", bytes, cudaGetErrorString(e));
+    }
+    *out = p;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_destroy(csemb_plan *p) {
+    if (!p) return CSEMB_OK;
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    cudaSetDevice(p->m->ctx->device);
+    cudaStreamSynchronize(p->m->ctx->stream);
+    plan_free(p);
+    return CSEMB_OK;
+}
+
+template <typename T>
+static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                      const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
+                      int64_t d_global, int normalize_rows) {
+    csemb_mat *m = p->m;
+    csemb_ctx *c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows;
+    const int d = (int)p->d, ld = (int)p->ld;
+    const int W = Vec<T>::W;
+    const int ldv = ld / W;
+    const int64_t n_chunks = (d_global + 31) / 32;
+    const size_t need = (size_t)n_stages * (size_t)std::max(order, 0) * (size_t)n_chunks;
+    if (need > p->peaks_cap) {
+        cudaFree(p->peaks);
+        p->peaks = nullptr;
+        p->peaks_cap = 0;
+        CK(cudaMalloc(&p->peaks, sizeof(unsigned long long) * need));
+        p->peaks_cap = need;
+    }
+    if (need) CK(cudaMemsetAsync(p->peaks, 0, sizeof(unsigned long long) * need, s));
+    p->order = order;
+    p->n_stages = n_stages;
+    p->n_chunks = n_chunks;
+    p->step_launches = 0;
+
+    T *y[2] = {(T *)p->y[0], (T *)p->y[1]};
+    T *E = (T *)p->E;
+    const double scale = 1.0 / std::sqrt((double)d_global);
+    const int gi = grid_for(n * (int64_t)ld, 256, c->sm_count, 16);
+    const int tiles = tiles_for(ldv);
+    CK(cudaEventRecord(p->ev[0], s));
+    for (int st = 0; st < n_stages; ++st) {
+        const int kind = st > 0 ? OMEGA_FROM_E : omega_kind;
+        if (n > 0)
+            k_stage_init<T><<<gi, 256, 0, s>>>(block_dev, y[0], E, n, d, ld, kind, seed, col0, d_global,
+                                               coeffs[0], scale);
+        CK(cudaGetLastError());
+        if (st == 0) CK(cudaEventRecord(p->ev[1], s));
+        for (int r = 1; r <= order; ++r) {
+            StepParams P;
+            P.rowptr = m->rowptr;
+            P.cols = m->cols;
+            P.vals = m->vals;
+            P.ycur = y[(r - 1) & 1];
+            P.yout = y[r & 1];
+            P.E = E;
+            P.n_rows = n;
+            P.ldv = ldv;
+            P.v0 = 0;
+            P.nvt = ldv;
+            P.alpha = 2.0 - 1.0 / (double)r;  // engine.py:214, same IEEE expression
+            P.beta = 1.0 - 1.0 / (double)r;   // engine.py:216
+            P.theta = coeffs[r];
+            P.has_prev = r > 1;
+            P.reverse = (r & 1) == 0;
+            P.peaks = p->peaks + ((size_t)st * order + (r - 1)) * n_chunks;
+            P.col0 = (int)col0;
+            if (n > 0) CK(launch_step<T, MODE_RECUR>(P, s, c->sm_count));
+            p->step_launches += tiles;
+        }
+        if (st == n_stages - 1) CK(cudaEventRecord(p->ev[2], s));
+        // the stage output lives in E; the next stage re-seeds Q(0) from it
+    }
+    if (normalize_rows && n > 0) {
+        k_rownorm<T><<<grid_for(n * 32, 256, c->sm_count, 8), 256, 0, s>>>(E, n, d, ld);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(p->ev[3], s));
+    p->ran = true;
+    return CSEMB_OK;
+}
+
+static int plan_run_locked(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                           const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
+                           int64_t d_global, int normalize_rows) {
+    if (!coeffs) return fail(CSEMB_ERR_INVALID, "null coefficients");
+    if (order < 0) return fail(CSEMB_ERR_INVALID, "order must be >= 0");
+    if (n_stages < 1) return fail(CSEMB_ERR_INVALID, "n_stages must be >= 1");
+    if (omega_kind < CSEMB_OMEGA_GIVEN || omega_kind > CSEMB_OMEGA_PHILOX)
+        return fail(CSEMB_ERR_INVALID, "unknown omega kind %d", omega_kind);
+    if (omega_kind == CSEMB_OMEGA_GIVEN && !block_dev && p->m->n_rows > 0)
+        return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
+    if (d_global < p->d || col0 < 0 || col0 + p->d > d_global)
+        return fail(CSEMB_ERR_INVALID, "column slice [%lld, %lld) outside d_global %lld", (long long)col0,
+                    (long long)(col0 + p->d), (long long)d_global);
+    if (col0 % vec_w(p->m->dtype) != 0)
+        return fail(CSEMB_ERR_INVALID, "col0 must be a multiple of %d", vec_w(p->m->dtype));
+    if (col0 > 0x7FFFFFFF) return fail(CSEMB_ERR_UNSUPPORTED, "col0 too large");
+    for (int r = 0; r <= order; ++r)
+        if (!std::isfinite(coeffs[r])) return fail(CSEMB_ERR_INVALID, "coefficients must be finite");
+    CK(cudaSetDevice(p->m->ctx->device));
+    if (p->m->dtype == CSEMB_F64)
+        return plan_run_t<double>(p, coeffs, order, n_stages, block_dev, omega_kind, seed, col0, d_global,
+                                  normalize_rows);
+    return plan_run_t<float>(p, coeffs, order, n_stages, block_dev, omega_kind, seed, col0, d_global,
+                             normalize_rows);
+}
+
+extern "C" int csemb_plan_run(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                              const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
+                              int64_t d_global, int normalize_rows) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    return plan_run_locked(p, coeffs, order, n_stages, block_dev, omega_kind, seed, col0, d_global,
+                           normalize_rows);
+}
+
+static int plan_download_locked(csemb_plan *p, void *out_host, int out_dtype) {
+    csemb_mat *m = p->m;
+    cudaStream_t s = m->ctx->stream;
+    const int64_t n = m->n_rows;
+    const int d = (int)p->d, ld = (int)p->ld;
+    if (n == 0) return CSEMB_OK;
+    const size_t osz = out_dtype == CSEMB_F32 ? 4 : 8;
+    if (osz == dsize(m->dtype)) {
+        CK(cudaMemcpy2DAsync(out_host, osz * d, p->E, osz * ld, osz * d, n, cudaMemcpyDeviceToHost, s));
+    } else {
+        // convert into the staging buffer (big enough for n x d f64), then copy
+        const size_t need = 8 * (size_t)n * (size_t)d;
+        if (p->staging_bytes < need) {
+            cudaFree(p->staging);
+            p->staging = nullptr;
+            p->staging_bytes = 0;
+            CK(cudaMalloc(&p->staging, need));
+            p->staging_bytes = need;
+        }
+        const int g = grid_for(n * (int64_t)d, 256, m->ctx->sm_count, 16);
+        if (m->dtype == CSEMB_F32)
+            k_unpack<float, double><<<g, 256, 0, s>>>((const float *)p->E, (double *)p->staging, n, d, ld);
+        else
+            k_unpack<double, float><<<g, 256, 0, s>>>((const double *)p->E, (float *)p->staging, n, d, ld);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out_host, p->staging, osz * (size_t)n * d, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_download(csemb_plan *p, void *out_host, int out_dtype) {
+    if (!p || !out_host) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (out_dtype != CSEMB_F64 && out_dtype != CSEMB_F32) return fail(CSEMB_ERR_INVALID, "bad out dtype");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    return plan_download_locked(p, out_host, out_dtype);
+}
+
+extern "C" int csemb_plan_output(csemb_plan *p, void **dev_ptr, int64_t *ld, int *dtype) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (dev_ptr) *dev_ptr = p->E;
+    if (ld) *ld = p->ld;
+    if (dtype) *dtype = p->m->dtype;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_copy_output(csemb_plan *p, void *dst_dev, int64_t dst_ld) {
+    if (!p || !dst_dev) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (dst_ld < p->d) return fail(CSEMB_ERR_INVALID, "dst_ld below d");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    if (p->m->n_rows == 0) return CSEMB_OK;
+    const size_t es = dsize(p->m->dtype);
+    CK(cudaMemcpy2DAsync(dst_dev, es * dst_ld, p->E, es * p->ld, es * p->d, p->m->n_rows,
+                         cudaMemcpyDeviceToDevice, p->m->ctx->stream));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_rownorm(csemb_ctx *c, void *E_dev, int64_t n, int64_t d, int64_t ld, int dtype) {
+    if (!c || (!E_dev && n > 0)) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (n < 0 || d < 0 || ld < d) return fail(CSEMB_ERR_INVALID, "bad block shape");
+    if (dtype != CSEMB_F64 && dtype != CSEMB_F32) return fail(CSEMB_ERR_INVALID, "bad dtype");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    if (n == 0 || d == 0) return CSEMB_OK;
+    const int g = grid_for(n * 32, 256, c->sm_count, 8);
+    if (dtype == CSEMB_F64)
+        k_rownorm<double><<<g, 256, 0, c->stream>>>((double *)E_dev, n, (int)d, (int)ld);
+    else
+        k_rownorm<float><<<g, 256, 0, c->stream>>>((float *)E_dev, n, (int)d, (int)ld);
+    CK(cudaGetLastError());
+    return CSEMB_OK;
+}
+
+static int plan_diag_locked(csemb_plan *p, double *max_abs, int *first_bad_r, int *bad_stage) {
+    cudaStream_t s = p->m->ctx->stream;
+    CK(cudaStreamSynchronize(s));
+    const size_t cnt = (size_t)p->n_stages * (size_t)p->order * (size_t)p->n_chunks;
+    std::vector<unsigned long long> h(cnt);
+    if (cnt) CK(cudaMemcpy(h.data(), p->peaks, 8 * cnt, cudaMemcpyDeviceToHost));
+    if (max_abs) std::memcpy(max_abs, h.data(), 8 * cnt);  // keys are |value| bit patterns
+    int fr = 0, fs = 0;
+    // reference order: stages in turn; within a stage, chunks in column order,
+    // each run to completion before the next (engine.py:250-252, 333-336)
+    for (int st = 0; st < p->n_stages && !fr; ++st)
+        for (int64_t ch = 0; ch < p->n_chunks && !fr; ++ch)
+            for (int r = 1; r <= p->order; ++r) {
+                const unsigned long long k = h[((size_t)st * p->order + (r - 1)) * p->n_chunks + ch];
+                if (k >= 0x7FF0000000000000ull) {
+                    fr = r;
+                    fs = st + 1;
+                    break;
+                }
+            }
+    if (first_bad_r) *first_bad_r = fr;
+    if (bad_stage) *bad_stage = fs;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_diagnostics(csemb_plan *p, double *max_abs, int *first_bad_r, int *bad_stage) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (!p->ran) return fail(CSEMB_ERR_INVALID, "plan has not run");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    return plan_diag_locked(p, max_abs, first_bad_r, bad_stage);
+}
+
+extern "C" int csemb_plan_timing(csemb_plan *p, float *ms_total, float *ms_steps, int *step_launches) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (!p->ran) return fail(CSEMB_ERR_INVALID, "plan has not run");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    CK(cudaEventSynchronize(p->ev[3]));
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, p->ev[0], p->ev[3]));
+    CK(cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
+    if (ms_total) *ms_total = a;
+    if (ms_steps) *ms_steps = b;
+    if (step_launches) *step_launches = p->step_launches;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int order, int n_stages,
+                                     const double *block_host, int omega_kind, uint64_t seed,
+                                     int64_t col0, int64_t d_global, int normalize_rows,
+                                     double *out_host, double *max_abs, int *first_bad_r, int *bad_stage) {
+    if (!p || !out_host) return fail(CSEMB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    csemb_mat *m = p->m;
+    CK(cudaSetDevice(m->ctx->device));
+    const int64_t n = m->n_rows;
+    const double *block_dev = nullptr;
+    if (omega_kind == CSEMB_OMEGA_GIVEN && n > 0) {
+        if (!block_host) return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
+        const size_t need = 8 * (size_t)n * (size_t)p->d;
+        if (p->staging_bytes < need) {
+            cudaFree(p->staging);
+            p->staging = nullptr;
+            p->staging_bytes = 0;
+            CK(cudaMalloc(&p->staging, need));
+            p->staging_bytes = need;
+        }
+        CK(cudaMemcpyAsync(p->staging, block_host, need, cudaMemcpyHostToDevice, m->ctx->stream));
+        block_dev = p->staging;
+    }
+    int rc = plan_run_locked(p, coeffs, order, n_stages, block_dev, omega_kind, seed, col0, d_global,
+                             normalize_rows);
+    if (rc) return rc;
+    int fr = 0, fs = 0;
+    rc = plan_diag_locked(p, max_abs, &fr, &fs);
+    if (rc) return rc;
+    if (first_bad_r) *first_bad_r = fr;
+    if (bad_stage) *bad_stage = fs;
+    rc = plan_download_locked(p, out_host, CSEMB_F64);
+    if (rc) return rc;
+    if (fr) return fail(CSEMB_ERR_DIVERGED, "iteration r=%d produced non-finite values (stage %d)", fr, fs);
+    return CSEMB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// projection block
+// ---------------------------------------------------------------------------
+extern "C" int csemb_sample_projection(csemb_ctx *c, int64_t n, int64_t d_global, uint64_t seed,
+                                       int64_t col0, int64_t w, int kind, double *out_host) {
+    if (!c || (!out_host && n * w > 0)) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (n < 1 || d_global < 1) return fail(CSEMB_ERR_INVALID, "projection shape must be positive");
+    if (col0 < 0 || w < 0 || col0 + w > d_global) return fail(CSEMB_ERR_INVALID, "column slice out of range");
+    if (kind != CSEMB_OMEGA_SPLITMIX && kind != CSEMB_OMEGA_PHILOX)
+        return fail(CSEMB_ERR_INVALID, "kind must be SPLITMIX or PHILOX");
+    std::lock_guard<std::mutex> lk(c->mu);
+    CK(cudaSetDevice(c->device));
+    if (w == 0) return CSEMB_OK;
+    double *buf = nullptr;
+    CK(cudaMalloc(&buf, 8 * (size_t)n * (size_t)w));
+    k_omega_dense<<<grid_for(n * w, 256, c->sm_count, 16), 256, 0, c->stream>>>(
+        buf, n, w, kind, seed, col0, d_global, 1.0 / std::sqrt((double)d_global));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out_host, buf, 8 * (size_t)n * (size_t)w, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(buf);
+    CK(e);
+    return CSEMB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// spectral norm (power iteration)
+// ---------------------------------------------------------------------------
+template <typename T>
+static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_host, uint64_t seed,
+                           double safety, double *out) {
+    csemb_ctx *c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows;
+    const int W = Vec<T>::W;
+    const int ld = (int)((k + W - 1) / W * W);
+    const int ldv = ld / W;
+    const int gy = std::min<int64_t>(std::max<int64_t>((n + 7) / 8, 1), 4 * c->sm_count);
+    const int gx = (int)((k + 31) / 32);
+    T *V = nullptr, *Wm = nullptr;
+    double *stage = nullptr, *partial = nullptr, *rq = nullptr, *inv = nullptr;
+    const size_t blk = sizeof(T) * (size_t)n * ld;
+    std::vector<double> hrq;
+    cudaError_t e = cudaMalloc(&V, blk);
+    if (e == cudaSuccess) e = cudaMalloc(&Wm, blk);
+    if (e == cudaSuccess) e = cudaMalloc(&partial, sizeof(double) * 2 * (size_t)gy * k);
+    if (e == cudaSuccess) e = cudaMalloc(&rq, sizeof(double) * (size_t)iters * k);
+    if (e == cudaSuccess) e = cudaMalloc(&inv, sizeof(double) * (size_t)k);
+    if (e == cudaSuccess && v0_host) {
+        e = cudaMalloc(&stage, sizeof(double) * (size_t)n * k);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(stage, v0_host, sizeof(double) * (size_t)n * k, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            k_pack<T><<<grid_for(n * (int64_t)ld, 256, c->sm_count, 16), 256, 0, s>>>(stage, V, n, (int)k, ld);
+            e = cudaGetLastError();
+        }
+    } else if (e == cudaSuccess) {
+        k_normal_init<T><<<grid_for(n * (int64_t)ld, 256, c->sm_count, 16), 256, 0, s>>>(V, n, (int)k, ld, seed);
+        e = cudaGetLastError();
+    }
+    const int gs = grid_for(n * (int64_t)ld, 256, c->sm_count, 16);
+    if (e == cudaSuccess) {
+        // V /= ||V||_col  (engine.py:181)
+        k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, nullptr, n, (int)k, ld, partial);
+        k_colfinish<<<(int)((k + 127) / 128), 128, 0, s>>>(partial, gy, (int)k, nullptr, inv);
+        k_colscale<T><<<gs, 256, 0, s>>>(V, V, inv, n, (int)k, ld);
+        e = cudaGetLastError();
+    }
+    for (int it = 0; it < iters && e == cudaSuccess; ++it) {
+        StepParams P;
+        std::memset(&P, 0, sizeof P);
+        P.rowptr = m->rowptr;
+        P.cols = m->cols;
+        P.vals = m->vals;
+        P.ycur = V;
+        P.yout = Wm;
+        P.n_rows = n;
+        P.ldv = ldv;
+        P.v0 = 0;
+        P.nvt = ldv;
+        e = launch_step<T, MODE_SPMM>(P, s, c->sm_count);  // W = S V (engine.py:184)
+        if (e != cudaSuccess) break;
+        // Rayleigh quotients and column norms (engine.py:185-187), then V = W / ||W|| (:191)
+        k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, Wm, n, (int)k, ld, partial);
+        k_colfinish<<<(int)((k + 127) / 128), 128, 0, s>>>(partial, gy, (int)k, rq + (size_t)it * k, inv);
+        k_colscale<T><<<gs, 256, 0, s>>>(V, Wm, inv, n, (int)k, ld);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        hrq.resize((size_t)iters * k);
+        e = cudaMemcpyAsync(hrq.data(), rq, sizeof(double) * hrq.size(), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    cudaFree(V);
+    cudaFree(Wm);
+    cudaFree(stage);
+    cudaFree(partial);
+    cudaFree(rq);
+    cudaFree(inv);
+    CK(e);
+    double best = 0.0;
+    for (double v : hrq) best = std::max(best, std::fabs(v));
+    *out = best * safety;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_spectral_norm(csemb_mat *m, int iters, int64_t k, const double *v0_host, uint64_t seed,
+                                   double safety, double *out) {
+    if (!m || !out) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (m->n_rows != m->n_cols)
+        return fail(CSEMB_ERR_INVALID, "spectral norm estimation requires a square matrix");
+    if (iters < 1 || k < 1 || !(safety >= 1.0)) return fail(CSEMB_ERR_INVALID, "bad norm-estimation settings");
+    if (k > 4096) return fail(CSEMB_ERR_UNSUPPORTED, "k above 4096");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    CK(cudaSetDevice(m->ctx->device));
+    if (m->nnz == 0) {  // engine.py:175-176
+        *out = 0.0;
+        return CSEMB_OK;
+    }
+    if (m->dtype == CSEMB_F64) return spectral_norm_t<double>(m, iters, k, v0_host, seed, safety, out);
+    return spectral_norm_t<float>(m, iters, k, v0_host, seed, safety, out);
+}

@@ -1,0 +1,508 @@
+// kernels.cuh -- sm_100a kernels of the fused SpMM-Legendre recurrence.
+//
+// K1 k_step      : one order of the recurrence (engine.py:213-227 + sparse.py:187)
+//                  Q(r) = alpha_r * (S Q(r-1)) - beta_r * Q(r-2);  E += theta_r Q(r)
+//                  fused: one pass over the CSR, the gathered rows of Q(r-1), and
+//                  the streamed rows of Q(r-2) (overwritten in place by Q(r)) and E.
+// K2 k_stage_init: projection block (engine.py:79-99 hash / Philox) or the previous
+//                  cascade stage's output, Q(0) = block, E = theta_0 * block
+//                  (engine.py:210-212).
+// K3 k_colstats / k_colfinish / k_colscale: power-iteration pieces for
+//                  estimate_spectral_norm (engine.py:180-191); SpMM via k_step<SPMM>.
+// K4 k_rownorm   : E_i / ||E_i|| with zero rows -> 0 (oracle.py:88-96 semantics).
+//
+// Layout: dense blocks are n x ld row-major, ld = d rounded up to one 16-byte
+// vector (double2 / float4); row r of a block is ld/W 16-byte vectors.
+// A row of the recurrence is owned by a group of G lanes; lane l handles the
+// 16-byte vectors l, l+G, l+2G, ... of the row (VPL of them), so every load of
+// a gathered row is a contiguous G*16-byte segment.
+//
+// fp64 arithmetic is strict: multiply and add are separately rounded
+// (__dmul_rn/__dadd_rn, no FMA contraction) and each output element is
+// accumulated over the row's stored entries in stored order starting from
+// +0.0, exactly as scipy's csr_matvecs and numpy do on the reference side --
+// so the fp64 path is bit-identical to the reference.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace csemb {
+
+enum { MODE_RECUR = 0, MODE_SPMM = 1 };
+
+template <typename T> struct Vec;
+template <> struct Vec<double> {
+    typedef double2 type;
+    static constexpr int W = 2;
+};
+template <> struct Vec<float> {
+    typedef float4 type;
+    static constexpr int W = 4;
+};
+
+__device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// acc + a*x, separately rounded (fp64 strict) / fused (fp32)
+__device__ __forceinline__ double2 vmadd(double2 acc, double a, double2 x) {
+    return make_double2(__dadd_rn(acc.x, __dmul_rn(a, x.x)), __dadd_rn(acc.y, __dmul_rn(a, x.y)));
+}
+__device__ __forceinline__ float4 vmadd(float4 acc, float a, float4 x) {
+    return make_float4(fmaf(a, x.x, acc.x), fmaf(a, x.y, acc.y), fmaf(a, x.z, acc.z),
+                       fmaf(a, x.w, acc.w));
+}
+
+// q = alpha*acc [- beta*p]  (numpy: q = alpha*y; q -= beta*q2)
+__device__ __forceinline__ double2 vrecur(double2 acc, double alpha, double beta, double2 p,
+                                          bool has_prev) {
+    double2 q = make_double2(__dmul_rn(alpha, acc.x), __dmul_rn(alpha, acc.y));
+    if (has_prev) {
+        q.x = __dsub_rn(q.x, __dmul_rn(beta, p.x));
+        q.y = __dsub_rn(q.y, __dmul_rn(beta, p.y));
+    }
+    return q;
+}
+__device__ __forceinline__ float4 vrecur(float4 acc, float alpha, float beta, float4 p,
+                                         bool has_prev) {
+    float4 q = make_float4(alpha * acc.x, alpha * acc.y, alpha * acc.z, alpha * acc.w);
+    if (has_prev) {
+        q.x = fmaf(-beta, p.x, q.x);
+        q.y = fmaf(-beta, p.y, q.y);
+        q.z = fmaf(-beta, p.z, q.z);
+        q.w = fmaf(-beta, p.w, q.w);
+    }
+    return q;
+}
+
+// e + theta*q  (numpy: acc += theta*q)
+__device__ __forceinline__ double2 vaccum(double2 e, double theta, double2 q) {
+    return make_double2(__dadd_rn(e.x, __dmul_rn(theta, q.x)), __dadd_rn(e.y, __dmul_rn(theta, q.y)));
+}
+__device__ __forceinline__ float4 vaccum(float4 e, float theta, float4 q) {
+    return make_float4(fmaf(theta, q.x, e.x), fmaf(theta, q.y, e.y), fmaf(theta, q.z, e.z),
+                       fmaf(theta, q.w, e.w));
+}
+
+// monotone key of |v| for max tracking; NaN > inf > finite, as np.max propagates NaN
+__device__ __forceinline__ unsigned long long absbits(double v) {
+    return (unsigned long long)__double_as_longlong(v) & 0x7FFFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ unsigned long long vpeak(double2 q) {
+    unsigned long long a = absbits(q.x), b = absbits(q.y);
+    return a > b ? a : b;
+}
+__device__ __forceinline__ unsigned long long vpeak(float4 q) {
+    unsigned int a = __float_as_uint(q.x) & 0x7FFFFFFFu, b = __float_as_uint(q.y) & 0x7FFFFFFFu;
+    unsigned int c = __float_as_uint(q.z) & 0x7FFFFFFFu, d = __float_as_uint(q.w) & 0x7FFFFFFFu;
+    a = a > b ? a : b;
+    c = c > d ? c : d;
+    a = a > c ? a : c;
+    // widen to the fp64 key so both precisions share one diagnostics format
+    return absbits((double)__uint_as_float(a));
+}
+
+// streaming (evict-first) accesses for data touched once per step
+template <typename V> __device__ __forceinline__ V ld_stream(const V *p) { return __ldcs(p); }
+template <typename V> __device__ __forceinline__ void st_stream(V *p, V v) { __stcs(p, v); }
+
+struct StepParams {
+    const int64_t *rowptr;
+    const int *cols;
+    const void *vals;
+    const void *ycur;  // Q(r-1): gathered
+    void *yout;        // in: Q(r-2) (if has_prev), out: Q(r)
+    void *E;           // accumulator (MODE_RECUR)
+    int64_t n_rows;
+    int ldv;           // row stride in 16-byte vectors
+    int v0;            // first vector of this column tile
+    int nvt;           // vectors in this column tile
+    double alpha, beta, theta;
+    int has_prev;
+    int reverse;       // sweep rows in descending order (L2 reuse of the tail)
+    unsigned long long *peaks;  // this step's per-chunk max|Q| keys (MODE_RECUR), or null
+    int col0;          // global column of vector 0 (for chunk ids)
+};
+
+// K1: one recurrence step (MODE_RECUR) or a plain multi-vector SpMM (MODE_SPMM).
+template <typename T, int G, int VPL, int MODE>
+__global__ void __launch_bounds__(256) k_step(const StepParams P) {
+    typedef typename Vec<T>::type VT;
+    constexpr int W = Vec<T>::W;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);  // lane within the row group
+    const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+
+    const T *__restrict__ vals = (const T *)P.vals;
+    const int *__restrict__ cols = P.cols;
+    const VT *__restrict__ ycur = (const VT *)P.ycur;
+    VT *yout = (VT *)P.yout;
+    VT *E = (VT *)P.E;
+    const T alpha = (T)P.alpha, beta = (T)P.beta, theta = (T)P.theta;
+    const bool has_prev = P.has_prev != 0;
+
+    bool valid[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) valid[k] = (gl + k * G) < P.nvt;
+    unsigned long long pk[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) pk[k] = 0ull;
+
+    for (int64_t it = gid; it < P.n_rows; it += ngroups) {
+        const int64_t row = P.reverse ? (P.n_rows - 1 - it) : it;
+        const int64_t beg = __ldg(P.rowptr + row), end = __ldg(P.rowptr + row + 1);
+        VT acc[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) acc[k] = vzero(VT());
+
+        // cooperative index/value fetch: lane t of the group holds entry base+t
+        int myj = 0;
+        T mya = (T)0;
+        if (beg + gl < end) {
+            myj = __ldcs(cols + beg + gl);
+            mya = __ldcs(vals + beg + gl);
+        }
+        for (int64_t base = beg; base < end; base += G) {
+            const int cnt = (int)((end - base) < G ? (end - base) : G);
+            int nj = 0;
+            T na = (T)0;
+            if (base + G + gl < end) {  // prefetch the next batch
+                nj = __ldcs(cols + base + G + gl);
+                na = __ldcs(vals + base + G + gl);
+            }
+            int t = 0;
+            for (; t + 1 < cnt; t += 2) {
+                const int j0 = __shfl_sync(gmask, myj, t, G);
+                const int j1 = __shfl_sync(gmask, myj, t + 1, G);
+                const T a0 = __shfl_sync(gmask, mya, t, G);
+                const T a1 = __shfl_sync(gmask, mya, t + 1, G);
+                const VT *x0 = ycur + (int64_t)j0 * P.ldv + P.v0 + gl;
+                const VT *x1 = ycur + (int64_t)j1 * P.ldv + P.v0 + gl;
+                VT b0[VPL], b1[VPL];
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    if (valid[k]) {
+                        b0[k] = __ldg(x0 + k * G);
+                        b1[k] = __ldg(x1 + k * G);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    if (valid[k]) {
+                        acc[k] = vmadd(acc[k], a0, b0[k]);  // stored order: t before t+1
+                        acc[k] = vmadd(acc[k], a1, b1[k]);
+                    }
+                }
+            }
+            if (t < cnt) {
+                const int j0 = __shfl_sync(gmask, myj, t, G);
+                const T a0 = __shfl_sync(gmask, mya, t, G);
+                const VT *x0 = ycur + (int64_t)j0 * P.ldv + P.v0 + gl;
+#pragma unroll
+                for (int k = 0; k < VPL; ++k)
+                    if (valid[k]) acc[k] = vmadd(acc[k], a0, __ldg(x0 + k * G));
+            }
+            myj = nj;
+            mya = na;
+        }
+
+        VT *yo = yout + row * (int64_t)P.ldv + P.v0 + gl;
+        if (MODE == MODE_SPMM) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k)
+                if (valid[k]) yo[k * G] = acc[k];
+        } else {
+            VT *er = E + row * (int64_t)P.ldv + P.v0 + gl;
+            VT pv[VPL], ev[VPL];
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                if (valid[k]) {
+                    pv[k] = has_prev ? ld_stream(yo + k * G) : vzero(VT());
+                    ev[k] = ld_stream(er + k * G);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                if (valid[k]) {
+                    const VT q = vrecur(acc[k], alpha, beta, pv[k], has_prev);
+                    yo[k * G] = q;
+                    st_stream(er + k * G, vaccum(ev[k], theta, q));
+                    const unsigned long long b = vpeak(q);
+                    pk[k] = b > pk[k] ? b : pk[k];
+                }
+            }
+        }
+    }
+
+    if (MODE == MODE_RECUR && P.peaks) {
+        // per-chunk max over the block, then one atomic per chunk per block
+        extern __shared__ unsigned long long s_peak[];
+        const int first_chunk = (P.col0 + P.v0 * W) >> 5;
+        const int last_chunk = (P.col0 + (P.v0 + P.nvt) * W - 1) >> 5;
+        const int nch = last_chunk - first_chunk + 1;
+        for (int c = threadIdx.x; c < nch; c += blockDim.x) s_peak[c] = 0ull;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            if (valid[k] && pk[k]) {
+                const int c = ((P.col0 + (P.v0 + gl + k * G) * W) >> 5) - first_chunk;
+                atomicMax(&s_peak[c], pk[k]);
+            }
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < nch; c += blockDim.x)
+            if (s_peak[c]) atomicMax(&P.peaks[first_chunk + c], s_peak[c]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: projection block / stage input
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Philox4x32-10 (Salmon et al., SC'11), returns output word 0
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const unsigned hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const unsigned hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+enum { OMEGA_GIVEN = 0, OMEGA_SPLITMIX = 1, OMEGA_PHILOX = 2, OMEGA_FROM_E = 3 };
+
+// sign of entry (i, gc) of the n x d_global projection: true => +1/sqrt(d)
+__device__ __forceinline__ bool omega_sign(int kind, uint64_t key, uint64_t seed, int64_t i,
+                                           int64_t gc, int64_t d_global) {
+    const uint64_t flat = (uint64_t)i * (uint64_t)d_global + (uint64_t)gc;
+    if (kind == OMEGA_SPLITMIX) return (mix64(flat ^ key) >> 63) != 0;
+    const uint4 r = philox4x32_10(make_uint4((unsigned)flat, (unsigned)(flat >> 32), 0u, 0u),
+                                  make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+    return (r.x >> 31) != 0;
+}
+
+// Q(0) = block, E = theta0 * block; pad columns [d, ld) are zero.
+template <typename T>
+__global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int64_t n, int d,
+                             int ld, int kind, uint64_t seed, int64_t col0, int64_t d_global,
+                             double theta0, double scale) {
+    const uint64_t key = mix64(seed);
+    const int64_t total = n * (int64_t)ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ld;
+        const int c = (int)(t - i * ld);
+        T v = (T)0, e = (T)0;
+        if (c < d) {
+            if (kind == OMEGA_FROM_E) {
+                v = E[t];
+            } else if (kind == OMEGA_GIVEN) {
+                v = (T)given[i * d + c];
+            } else {
+                v = (T)(omega_sign(kind, key, seed, i, col0 + c, d_global) ? scale : -scale);
+            }
+            if (sizeof(T) == 8)
+                e = (T)__dmul_rn((double)theta0, (double)v);
+            else
+                e = (T)theta0 * v;
+        }
+        y0[t] = v;
+        E[t] = e;
+    }
+}
+
+// dense n x w projection (f64 out) for sample_projection
+__global__ void k_omega_dense(double *out, int64_t n, int64_t w, int kind, uint64_t seed,
+                              int64_t col0, int64_t d_global, double scale) {
+    const uint64_t key = mix64(seed);
+    const int64_t total = n * w;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / w;
+        const int64_t c = t - i * w;
+        out[t] = omega_sign(kind, key, seed, i, col0 + c, d_global) ? scale : -scale;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4: row normalisation, one warp per row
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_rownorm(T *E, int64_t n, int d, int ld) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nw) {
+        T *r = E + i * ld;
+        double s = 0.0;
+        for (int c = lane; c < d; c += 32) {
+            const double v = (double)r[c];
+            s += v * v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        const double nrm = sqrt(s);
+        for (int c = lane; c < d; c += 32) r[c] = nrm > 0.0 ? (T)((double)r[c] / nrm) : (T)0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: column statistics for the power iteration
+// ---------------------------------------------------------------------------
+// partial[(by*2+0)*k + c] = sum_rows V[r,c]*W[r,c]; partial[(by*2+1)*k + c] = sum W[r,c]^2
+// (W == null: sum V^2 only, into slot 1).  blockDim = (32, 8).
+template <typename T>
+__global__ void k_colstats(const T *__restrict__ V, const T *__restrict__ Wm, int64_t n, int k,
+                           int ld, double *partial) {
+    __shared__ double s_dot[8][33], s_sq[8][33];
+    const int c = blockIdx.x * 32 + threadIdx.x;
+    double dot = 0.0, sq = 0.0;
+    if (c < k) {
+        for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < n; r += (int64_t)gridDim.y * 8) {
+            const double v = (double)V[r * ld + c];
+            if (Wm) {
+                const double w = (double)Wm[r * ld + c];
+                dot += v * w;
+                sq += w * w;
+            } else {
+                sq += v * v;
+            }
+        }
+    }
+    s_dot[threadIdx.y][threadIdx.x] = dot;
+    s_sq[threadIdx.y][threadIdx.x] = sq;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < k) {
+        double a = 0.0, b = 0.0;
+        for (int y = 0; y < 8; ++y) {
+            a += s_dot[y][threadIdx.x];
+            b += s_sq[y][threadIdx.x];
+        }
+        partial[((int64_t)blockIdx.y * 2 + 0) * k + c] = a;
+        partial[((int64_t)blockIdx.y * 2 + 1) * k + c] = b;
+    }
+}
+
+// fixed-order sum of the partials: rq[c] = dot, inv[c] = 1/sqrt(sq) (0 if sq == 0)
+__global__ void k_colfinish(const double *partial, int nparts, int k, double *rq, double *inv) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double a = 0.0, b = 0.0;
+    for (int p = 0; p < nparts; ++p) {
+        a += partial[((int64_t)p * 2 + 0) * k + c];
+        b += partial[((int64_t)p * 2 + 1) * k + c];
+    }
+    if (rq) rq[c] = a;
+    const double nrm = sqrt(b);
+    inv[c] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+}
+
+// dst[r,c] = src[r,c] * inv[c]  (dead columns become 0, like dropping them)
+template <typename T>
+__global__ void k_colscale(T *dst, const T *src, const double *inv, int64_t n, int k, int ld) {
+    const int64_t total = n * (int64_t)ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(t % ld);
+        dst[t] = c < k ? (T)((double)src[t] * inv[c]) : (T)0;
+    }
+}
+
+// standard normals from Philox (Box-Muller) for the power-iteration start block
+template <typename T>
+__global__ void k_normal_init(T *V, int64_t n, int k, int ld, uint64_t seed) {
+    const int64_t total = n * (int64_t)ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ld;
+        const int c = (int)(t - i * ld);
+        T v = (T)0;
+        if (c < k) {
+            const uint64_t flat = (uint64_t)i * (uint64_t)k + (uint64_t)c;
+            const uint4 r = philox4x32_10(make_uint4((unsigned)flat, (unsigned)(flat >> 32), 0x6E6F726Du, 0u),
+                                          make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+            const double u1 = ((double)r.x + 1.0) * 2.3283064365386963e-10;  // (0, 1]
+            const double u2 = (double)r.y * 2.3283064365386963e-10;
+            v = (T)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+        }
+        V[t] = v;
+    }
+}
+
+// f64 -> T with row padding (n x d dense -> n x ld)
+template <typename T>
+__global__ void k_pack(const double *__restrict__ src, T *dst, int64_t n, int d, int ld) {
+    const int64_t total = n * (int64_t)ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ld;
+        const int c = (int)(t - i * ld);
+        dst[t] = c < d ? (T)src[i * d + c] : (T)0;
+    }
+}
+
+// n x ld (T) -> n x d (f64 or f32) without padding
+template <typename T, typename O>
+__global__ void k_unpack(const T *__restrict__ src, O *dst, int64_t n, int d, int ld) {
+    const int64_t total = n * (int64_t)d;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / d;
+        const int c = (int)(t - i * d);
+        dst[t] = (O)src[i * ld + c];
+    }
+}
+
+// CSR conversion: int64 -> int32 column indices (with range check), f64 -> T values
+__global__ void k_cols_to_i32(const int64_t *__restrict__ src, int *dst, int64_t cnt,
+                              int64_t n_cols, int *bad) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = src[t];
+        if (v < 0 || v >= n_cols) atomicExch(bad, 1);
+        dst[t] = (int)v;
+    }
+}
+__global__ void k_cols_check_i32(const int *__restrict__ src, int *dst, int64_t cnt,
+                                 int64_t n_cols, int *bad) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int v = src[t];
+        if (v < 0 || (int64_t)v >= n_cols) atomicExch(bad, 1);
+        dst[t] = v;
+    }
+}
+template <typename T>
+__global__ void k_vals_convert(const double *__restrict__ src, T *dst, int64_t cnt) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = (T)src[t];
+}
+template <typename T>
+__global__ void k_vals_scale(T *v, int64_t cnt, double factor) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        if (sizeof(T) == 8)
+            v[t] = (T)__dmul_rn((double)v[t], factor);
+        else
+            v[t] = (T)((double)v[t] * factor);
+    }
+}
+template <typename T>
+__global__ void k_vals_to_f64(const T *__restrict__ v, double *out, int64_t cnt) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+         t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = (double)v[t];
+}
+
+}  // namespace csemb

@@ -1,0 +1,557 @@
+"""Embedding engine: the reference's public API over the B200 device path.
+
+Drop-in for the reference `csemb` engine (engine.py): same function names,
+signatures, argument meaning, provenance keys and exceptions.  Everything
+between the host arrays and the result runs on the GPU through the C ABI
+(include/csemb_cuda.h, libcsemb_cuda.so):
+
+  fast_embed_eig / fast_embed_cascaded / fast_embed_general (engine.py:261-391)
+    -> apply_expansion (the seam, engine.py:231-258)
+       -> csemb_apply_expansion: K2 projection/stage init, L x K1 fused
+          SpMM-recurrence steps, optional K4 row normalisation.
+  sample_projection (engine.py:79-99)       -> csemb_sample_projection (K2)
+  estimate_spectral_norm (engine.py:165-192) -> csemb_spectral_norm (K3)
+
+Additive keywords (defaults reproduce the reference bit-for-bit):
+  dtype="float64"|"float32", normalize_rows=False, device=0,
+  omega_kind="reference"|"philox" (only where the engine samples Omega itself),
+  start="reference"|"philox" (norm-estimate starting block).
+`n_workers` is accepted and ignored, as the reference guarantees results are
+independent of it (tests/test_engine.py:162-171).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import logging
+import math
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import DivergenceError
+from .functions import describe, odd_extension, root_function
+from .legendre import LegendreExpansion, legendre_coefficients
+from .sparse import SparseMatrix, dilate
+
+logger = logging.getLogger("csemb.engine")  # the reference's logger name (engine.py:33)
+
+COLUMN_CHUNK = 32
+NORM_SEED_TAG = 0x6E6F726D  # "norm" (engine.py:36)
+_M64 = (1 << 64) - 1
+
+
+# ---------------------------------------------------------------------------
+# seeds and dimensions (host arithmetic)
+# ---------------------------------------------------------------------------
+def _mix64(z: int) -> int:
+    """SplitMix64 finalizer on Python ints (engine.py:44-50)."""
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def fold_seed(seed: int, index: int) -> int:
+    """Decorrelated sub-seed (engine.py:53-56)."""
+    return _mix64(((seed & _M64) + (index & _M64)) & _M64)
+
+
+def jl_dimension(n: int, epsilon: float, beta: float) -> int:
+    """Smallest d above (4 + 2 beta) ln n / (eps^2/2 - eps^3/3) (engine.py:59-68)."""
+    if n < 2:
+        raise ValueError("n must be >= 2")
+    if not 0.0 < epsilon < 1.0:
+        raise ValueError("epsilon must lie in (0, 1)")
+    if not beta > 0.0:
+        raise ValueError("beta must be positive")
+    bound = (4.0 + 2.0 * beta) * math.log(n) / (epsilon**2 / 2.0 - epsilon**3 / 3.0)
+    return math.floor(bound) + 1
+
+
+def default_dimension(n: int) -> int:
+    """ceil(6 ln n) (engine.py:71-76)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    return max(1, math.ceil(6.0 * math.log(n)))
+
+
+@dataclass(frozen=True)
+class EmbedConfig:
+    """Parameters of one embedding run (engine.py:102-138)."""
+
+    L: int
+    d: int
+    b: int = 1
+    seed: int = 0
+    epsilon: float = 0.5
+    beta: float = 1.0
+    norm_iters: int = 20
+    norm_vectors_factor: float = 6.0
+    norm_safety: float = 1.01
+
+    def __post_init__(self):
+        if self.L < 1:
+            raise ValueError("L must be >= 1")
+        if self.b < 1 or self.L % self.b != 0:
+            raise ValueError("b must be >= 1 and divide L")
+        if self.d < 1:
+            raise ValueError("d must be >= 1")
+        if not 0.0 < self.epsilon < 1.0:
+            raise ValueError("epsilon must lie in (0, 1)")
+        if not self.beta > 0.0:
+            raise ValueError("beta must be positive")
+        if self.norm_iters < 1 or self.norm_vectors_factor <= 0 or self.norm_safety < 1:
+            raise ValueError("bad norm-estimation settings")
+
+    @property
+    def stage_order(self) -> int:
+        return self.L // self.b
+
+
+@dataclass
+class SpmvCounter:
+    """Logical multi-vector products, one per recursion step (engine.py:141-145)."""
+
+    products: int = 0
+
+
+@dataclass
+class EmbeddingMatrix:
+    """Embedding rows plus provenance (engine.py:148-162)."""
+
+    values: np.ndarray
+    row_labels: np.ndarray | None = None
+    provenance: dict = field(default_factory=dict)
+
+    @property
+    def n_rows(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.values.shape[1]
+
+
+# ---------------------------------------------------------------------------
+# device handles
+# ---------------------------------------------------------------------------
+_DTYPES = {"float64": _lib.F64, "f64": _lib.F64, "fp64": _lib.F64, np.float64: _lib.F64,
+           "float32": _lib.F32, "f32": _lib.F32, "fp32": _lib.F32, np.float32: _lib.F32}
+_OMEGA = {"reference": _lib.OMEGA_SPLITMIX, "splitmix": _lib.OMEGA_SPLITMIX,
+          "philox": _lib.OMEGA_PHILOX}
+
+
+def dtype_code(dtype) -> int:
+    try:
+        return _DTYPES[dtype]
+    except (KeyError, TypeError):
+        raise ValueError(f"dtype must be float64 or float32, not {dtype!r}") from None
+
+
+class DeviceMatrix:
+    """A CSR matrix resident on one GPU (csemb_mat): int64 row offsets, int32
+    column indices, values in the run dtype.  Owns its plans."""
+
+    def __init__(self, S, dtype="float64", device: int = 0, *, _handle=None):
+        self.ctx = _lib.context(device)
+        self.lib = self.ctx.lib
+        self.dtype = dtype_code(dtype)
+        if _handle is not None:
+            self.handle = _handle
+        else:
+            S = SparseMatrix.of(S)
+            h = C.c_void_p()
+            _lib.check(self.lib.csemb_matrix_upload(
+                self.ctx.handle, S.n_rows, S.n_cols, S.nnz, _lib.ptr(S.row_offsets),
+                _lib.ptr(S.col_indices), _lib.ptr(S.values), self.dtype, C.byref(h)),
+                "csemb_matrix_upload")
+            self.handle = h
+        nr, nc, nz, dt = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        _lib.check(self.lib.csemb_matrix_info(self.handle, C.byref(nr), C.byref(nc), C.byref(nz),
+                                              C.byref(dt)))
+        self.n_rows, self.n_cols, self.nnz = int(nr.value), int(nc.value), int(nz.value)
+        self._plans: dict[int, Plan] = {}
+
+    @classmethod
+    def from_device(cls, n_rows, n_cols, nnz, row_offsets_ptr, col_indices_ptr, idx_bytes,
+                    values_ptr, dtype="float64", device: int = 0) -> "DeviceMatrix":
+        """Adopt a CSR already in device memory (e.g. built by torch on the GPU)."""
+        ctx = _lib.context(device)
+        h = C.c_void_p()
+        _lib.check(ctx.lib.csemb_matrix_upload_device(
+            ctx.handle, n_rows, n_cols, nnz, C.c_void_p(row_offsets_ptr), C.c_void_p(col_indices_ptr),
+            idx_bytes, C.c_void_p(values_ptr), dtype_code(dtype), C.byref(h)),
+            "csemb_matrix_upload_device")
+        return cls(None, dtype, device, _handle=h)
+
+    def scale(self, factor: float) -> None:
+        """values *= factor in place (scale_values, sparse.py:295-301)."""
+        _lib.check(self.lib.csemb_matrix_scale(self.handle, float(factor)), "csemb_matrix_scale")
+
+    def download_values(self) -> np.ndarray:
+        out = np.empty(self.nnz, dtype=np.float64)
+        _lib.check(self.lib.csemb_matrix_download_values(self.handle, _lib.ptr(out)))
+        return out
+
+    def plan(self, d: int) -> "Plan":
+        p = self._plans.get(d)
+        if p is None:
+            p = self._plans[d] = Plan(self, d)
+        return p
+
+    def release_plans(self) -> None:
+        for p in self._plans.values():
+            p.close()
+        self._plans.clear()
+
+    def close(self) -> None:
+        self.release_plans()
+        if self.handle:
+            self.lib.csemb_matrix_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plan:
+    """Device workspace (Q buffers, E, diagnostics) for one (matrix, d)."""
+
+    def __init__(self, dm: DeviceMatrix, d: int):
+        self.dm = dm
+        self.lib = dm.lib
+        self.d = int(d)
+        h = C.c_void_p()
+        _lib.check(self.lib.csemb_plan_create(dm.handle, self.d, C.byref(h)), "csemb_plan_create")
+        self.handle = h
+        self.last = None
+
+    def run(self, coeffs, n_stages: int = 1, *, block_dev: int | None = None, omega_kind: int = _lib.OMEGA_SPLITMIX,
+            seed: int = 0, col0: int = 0, d_global: int | None = None, normalize_rows: bool = False) -> None:
+        """Asynchronous device-resident run (csemb_plan_run)."""
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        d_global = self.d if d_global is None else int(d_global)
+        _lib.check(self.lib.csemb_plan_run(
+            self.handle, _lib.ptr(c), len(c) - 1, int(n_stages),
+            None if block_dev is None else C.c_void_p(block_dev), int(omega_kind), int(seed) & _M64,
+            int(col0), d_global, int(bool(normalize_rows))), "csemb_plan_run")
+        self.last = (len(c) - 1, int(n_stages), d_global, int(col0))
+
+    def apply(self, coeffs, n_stages: int, block: np.ndarray | None, *, omega_kind=_lib.OMEGA_GIVEN,
+              seed: int = 0, col0: int = 0, d_global: int | None = None, normalize_rows: bool = False,
+              out: np.ndarray | None = None) -> np.ndarray:
+        """Host-to-host run (csemb_apply_expansion); raises DivergenceError."""
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        order = len(c) - 1
+        n = self.dm.n_rows
+        d_global = self.d if d_global is None else int(d_global)
+        if block is not None:
+            block = np.ascontiguousarray(block, dtype=np.float64)
+            if block.shape != (n, self.d):
+                raise ValueError("projection block must be 2-d with one row per vertex")
+        if out is None:
+            out = np.empty((n, self.d), dtype=np.float64)
+        n_chunks = (d_global + COLUMN_CHUNK - 1) // COLUMN_CHUNK
+        peaks = np.zeros(max(n_stages * order * n_chunks, 1), dtype=np.uint64)
+        bad_r, bad_stage = C.c_int(0), C.c_int(0)
+        rc = self.lib.csemb_apply_expansion(
+            self.handle, _lib.ptr(c), order, int(n_stages), _lib.ptr(block), int(omega_kind),
+            int(seed) & _M64, int(col0), d_global, int(bool(normalize_rows)), _lib.ptr(out),
+            _lib.ptr(peaks), C.byref(bad_r), C.byref(bad_stage))
+        self.last = (order, int(n_stages), d_global, int(col0))
+        self.peaks = peaks[: n_stages * order * n_chunks].view(np.float64).reshape(n_stages, order, n_chunks)
+        if rc == _lib.ERR_DIVERGED:
+            raise DivergenceError(_lib.DIVERGENCE_MESSAGE.format(r=int(bad_r.value)))
+        _lib.check(rc, "csemb_apply_expansion")
+        return out
+
+    def download(self, out_dtype=np.float64) -> np.ndarray:
+        code = dtype_code(np.dtype(out_dtype).type)
+        out = np.empty((self.dm.n_rows, self.d), dtype=out_dtype)
+        _lib.check(self.lib.csemb_plan_download(self.handle, _lib.ptr(out), code), "csemb_plan_download")
+        return out
+
+    def output(self) -> tuple[int, int, int]:
+        """(device pointer, ld in elements, dtype code) of E."""
+        p, ld, dt = C.c_void_p(), C.c_int64(), C.c_int()
+        _lib.check(self.lib.csemb_plan_output(self.handle, C.byref(p), C.byref(ld), C.byref(dt)))
+        return int(p.value or 0), int(ld.value), int(dt.value)
+
+    def copy_output_to(self, dst_ptr: int, dst_ld: int) -> None:
+        """Device-to-device copy of E into a caller buffer (e.g. a torch tensor)."""
+        _lib.check(self.lib.csemb_plan_copy_output(self.handle, C.c_void_p(dst_ptr), int(dst_ld)),
+                   "csemb_plan_copy_output")
+
+    def diagnostics(self) -> tuple[np.ndarray, int, int]:
+        """(max|Q(r)| per stage/step/chunk, first bad r, its stage)."""
+        order, n_stages, d_global, _ = self.last
+        n_chunks = (d_global + COLUMN_CHUNK - 1) // COLUMN_CHUNK
+        peaks = np.zeros(max(n_stages * order * n_chunks, 1), dtype=np.uint64)
+        r, st = C.c_int(0), C.c_int(0)
+        _lib.check(self.lib.csemb_plan_diagnostics(self.handle, _lib.ptr(peaks), C.byref(r), C.byref(st)))
+        return (peaks[: n_stages * order * n_chunks].view(np.float64).reshape(n_stages, order, n_chunks),
+                int(r.value), int(st.value))
+
+    def timing(self) -> tuple[float, float, int]:
+        """(ms whole run, ms recurrence steps, K1 launches) from CUDA events."""
+        a, b, k = C.c_float(), C.c_float(), C.c_int()
+        _lib.check(self.lib.csemb_plan_timing(self.handle, C.byref(a), C.byref(b), C.byref(k)))
+        return float(a.value), float(b.value), int(k.value)
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.csemb_plan_destroy(self.handle)
+            self.handle = None
+
+
+_device_cache: dict[tuple, tuple] = {}
+
+
+def device_matrix(S, dtype="float64", device: int = 0) -> DeviceMatrix:
+    """The cached device copy of S (uploaded on first use, freed with S)."""
+    if isinstance(S, DeviceMatrix):
+        return S
+    key = (id(S), dtype_code(dtype), int(device))
+    hit = _device_cache.get(key)
+    if hit is not None:
+        ref, dm = hit
+        if ref() is S:
+            return dm
+    dm = DeviceMatrix(S, dtype, device)
+    try:
+        ref = weakref.ref(S)
+        weakref.finalize(S, _device_cache.pop, key, None)
+    except TypeError:  # not weak-referenceable: do not cache
+        return dm
+    _device_cache[key] = (ref, dm)
+    return dm
+
+
+# ---------------------------------------------------------------------------
+# the seam and the public entry points
+# ---------------------------------------------------------------------------
+def _resolve_expansion(f, order: int, quadrature) -> LegendreExpansion:
+    """engine.py:195-202."""
+    if hasattr(f, "coeffs") and hasattr(f, "order") and not callable(f):
+        if f.order != order:
+            raise ValueError(f"expansion order {f.order} does not match requested order {order}")
+        return f
+    return legendre_coefficients(f, order, quadrature)
+
+
+def _log_steps(peaks: np.ndarray, d: int, col_base: int = 0) -> None:
+    """Replay the reference's per-step debug records (engine.py:218-220)."""
+    if not logger.isEnabledFor(logging.DEBUG):
+        return
+    n_stages, order, n_chunks = peaks.shape
+    for st in range(n_stages):
+        for ch in range(n_chunks):
+            lo = ch * COLUMN_CHUNK
+            w = min(lo + COLUMN_CHUNK, d) - lo
+            for r in range(1, order + 1):
+                logger.debug("stage=%d cols=%d+%d r=%d max_abs=%.6e", st + 1, col_base + lo, w, r,
+                             float(peaks[st, r - 1, ch]))
+
+
+def _run(S, coeffs, n_stages, block, *, dtype, device, normalize_rows, omega_kind=_lib.OMEGA_GIVEN,
+         seed=0, d=None):
+    if S.n_rows != S.n_cols:
+        raise ValueError("the recurrence requires a square (symmetric) matrix")
+    dm = device_matrix(S, dtype, device)
+    d = block.shape[1] if block is not None else int(d)
+    out = dm.plan(d).apply(coeffs, n_stages, block, omega_kind=omega_kind, seed=seed,
+                           normalize_rows=normalize_rows)
+    _log_steps(dm.plan(d).peaks, d)
+    return out
+
+
+def apply_expansion(S, expansion, block, *, stage: int = 0, n_workers: int = 1, counter=None,
+                    dtype="float64", device: int = 0, normalize_rows: bool = False) -> np.ndarray:
+    """The drop-in seam: engine._apply_expansion (engine.py:231-258) on the GPU."""
+    block = np.asarray(block, dtype=np.float64)
+    if block.ndim != 2 or block.shape[0] != S.n_rows:
+        raise ValueError("projection block must be 2-d with one row per vertex")
+    out = _run(S, expansion.coeffs, 1, block, dtype=dtype, device=device, normalize_rows=normalize_rows)
+    if counter is not None:
+        counter.products += expansion.order
+    return out
+
+
+_apply_expansion = apply_expansion  # the reference's private name, for install()
+
+
+def fast_embed_eig(S, f, L: int, omega, *, quadrature=None, n_workers: int = 1, counter=None,
+                   dtype="float64", device: int = 0, normalize_rows: bool = False) -> EmbeddingMatrix:
+    """f_L(S) @ omega for symmetric S with ||S|| <= 1 (engine.py:261-299)."""
+    if S.n_rows != S.n_cols:
+        raise ValueError("fast_embed_eig requires a square (symmetric) matrix")
+    omega = np.asarray(omega, dtype=np.float64)
+    if omega.ndim != 2 or omega.shape[0] != S.n_rows:
+        raise ValueError("projection block must be 2-d with one row per vertex")
+    if L < 0:
+        raise ValueError("L must be >= 0")
+    expansion = _resolve_expansion(f, L, quadrature)
+    own = counter if counter is not None else SpmvCounter()
+    values = apply_expansion(S, expansion, omega, stage=1, counter=own, dtype=dtype, device=device,
+                             normalize_rows=normalize_rows)
+    return EmbeddingMatrix(values=values, provenance={
+        "function": _describe(f), "L": L, "b": 1, "d": omega.shape[1],
+        "spmv_products": own.products, "coeffs_sha256": expansion.digest()})
+
+
+def fast_embed_cascaded(S, f, cfg: EmbedConfig, omega=None, *, quadrature=None, n_workers: int = 1,
+                        counter=None, dtype="float64", device: int = 0, normalize_rows: bool = False,
+                        omega_kind: str = "reference") -> EmbeddingMatrix:
+    """b cascade stages of order L/b on the b-th root of f (engine.py:302-349).
+
+    With omega=None the projection is generated on the device (the reference's
+    SplitMix64 hash, bit-identical, or Philox with omega_kind="philox")."""
+    if S.n_rows != S.n_cols:
+        raise ValueError("fast_embed_cascaded requires a square (symmetric) matrix")
+    kind = _lib.OMEGA_GIVEN
+    if omega is None:
+        if omega_kind not in _OMEGA:
+            raise ValueError(f"omega_kind must be one of {sorted(_OMEGA)}")
+        kind = _OMEGA[omega_kind]
+        if S.n_rows < 1:
+            raise ValueError("projection shape must be positive")
+    else:
+        omega = np.asarray(omega, dtype=np.float64)
+        if omega.ndim != 2 or omega.shape[0] != S.n_rows:
+            raise ValueError("projection block must be 2-d with one row per vertex")
+    d = cfg.d if omega is None else omega.shape[1]
+    if cfg.b == 1:
+        g = f
+    else:
+        if hasattr(f, "coeffs") and not callable(f):
+            raise ValueError("cascading needs the function itself, not an expansion")
+        g = root_function(f, cfg.b)
+    expansion = _resolve_expansion(g, cfg.stage_order, quadrature)
+    own = counter if counter is not None else SpmvCounter()
+    values = _run(S, expansion.coeffs, cfg.b, omega, dtype=dtype, device=device,
+                  normalize_rows=normalize_rows, omega_kind=kind, seed=cfg.seed, d=d)
+    own.products += expansion.order * cfg.b
+    return EmbeddingMatrix(values=values, provenance={
+        "function": _describe(f), "L": cfg.L, "b": cfg.b, "stage_order": cfg.stage_order, "d": d,
+        "seed": cfg.seed, "spmv_products": own.products, "coeffs_sha256": expansion.digest()})
+
+
+def fast_embed_general(A, f, cfg: EmbedConfig, *, quadrature=None, n_workers: int = 1, counter=None,
+                       dtype="float64", device: int = 0, normalize_rows: bool = False,
+                       omega_kind: str = "reference"):
+    """Row and column embeddings of a rectangular A via the dilation
+    [0 A^T; A 0] and the odd extension of f (engine.py:352-391)."""
+    S = dilate(A)
+    m, n = A.n_rows, A.n_cols
+    emb = fast_embed_cascaded(S, odd_extension(f), cfg, None, quadrature=quadrature, counter=counter,
+                              dtype=dtype, device=device, normalize_rows=normalize_rows,
+                              omega_kind=omega_kind)
+    emb.provenance["function"] = _describe(odd_extension(f))
+    base = dict(emb.provenance)
+    rows = EmbeddingMatrix(values=emb.values[n:], row_labels=np.arange(m, dtype=np.int64),
+                           provenance={**base, "side": "rows"})
+    cols = EmbeddingMatrix(values=emb.values[:n], row_labels=np.arange(n, dtype=np.int64),
+                           provenance={**base, "side": "columns"})
+    return rows, cols
+
+
+def sample_projection(n: int, d: int, seed: int, *, kind: str = "reference", col0: int = 0,
+                      w: int | None = None, device: int = 0) -> np.ndarray:
+    """n x d block of +-1/sqrt(d), generated on the device (engine.py:79-99).
+    kind="reference" is bit-identical to the reference; col0/w select a column
+    slice hashed with the global d."""
+    if n < 1 or d < 1:
+        raise ValueError("projection shape must be positive")
+    if kind not in _OMEGA:
+        raise ValueError(f"kind must be one of {sorted(_OMEGA)}")
+    w = d - col0 if w is None else int(w)
+    ctx = _lib.context(device)
+    out = np.empty((n, w), dtype=np.float64)
+    _lib.check(ctx.lib.csemb_sample_projection(ctx.handle, n, d, int(seed) & _M64, col0, w, _OMEGA[kind],
+                                               _lib.ptr(out)), "csemb_sample_projection")
+    return out
+
+
+def norm_start_block(n: int, cfg: EmbedConfig) -> np.ndarray:
+    """The reference's PCG64 starting block (engine.py:178-180)."""
+    k = max(1, math.ceil(cfg.norm_vectors_factor * math.log(max(n, 2))))
+    return np.random.default_rng(fold_seed(cfg.seed, NORM_SEED_TAG)).standard_normal((n, k))
+
+
+def estimate_spectral_norm(S, cfg: EmbedConfig, *, start: str = "reference", dtype="float64",
+                           device: int = 0) -> float:
+    """Power-iteration estimate of ||S|| on the device (engine.py:165-192).
+
+    start="reference" uploads the reference's PCG64 starting block so the
+    estimate matches the reference to rounding; "philox" draws the normals on
+    the device (no host work, for large n)."""
+    if S.n_rows != S.n_cols:
+        raise ValueError("spectral norm estimation requires a square matrix")
+    if S.nnz == 0:
+        return 0.0
+    n = S.n_rows
+    k = max(1, math.ceil(cfg.norm_vectors_factor * math.log(max(n, 2))))
+    v0 = None
+    if start == "reference":
+        v0 = np.ascontiguousarray(norm_start_block(n, cfg))
+    elif start != "philox":
+        raise ValueError("start must be 'reference' or 'philox'")
+    dm = device_matrix(S, dtype, device)
+    out = C.c_double(0.0)
+    _lib.check(dm.lib.csemb_spectral_norm(dm.handle, cfg.norm_iters, k, _lib.ptr(v0),
+                                          fold_seed(cfg.seed, NORM_SEED_TAG), cfg.norm_safety,
+                                          C.byref(out)), "csemb_spectral_norm")
+    return float(out.value)
+
+
+def _describe(f) -> str:
+    if hasattr(f, "coeffs") and hasattr(f, "order") and not callable(f):
+        return f"expansion[{f.order}]"
+    return describe(f)
+
+
+def install(csemb_module):
+    """Rebind the reference package's seam (and Omega / norm entry points) to
+    the device path, so the reference's own drivers, tests and CLI run on the
+    GPU.  Returns a callable that restores the originals."""
+    import importlib
+
+    saved = []
+
+    def patch(mod, name, fn):
+        if hasattr(mod, name):
+            saved.append((mod, name, getattr(mod, name)))
+            setattr(mod, name, fn)
+
+    def seam(S, expansion, block, *, stage=0, n_workers=1, counter=None):
+        return apply_expansion(S, expansion, block, stage=stage, counter=counter)
+
+    def norm(S, cfg):
+        return estimate_spectral_norm(S, cfg)
+
+    def proj(n, d, seed):
+        return sample_projection(n, d, seed)
+
+    base = csemb_module.__name__
+    for sub in ("engine", "oracle", "cli", "cluster"):
+        try:
+            mod = importlib.import_module(f"{base}.{sub}")
+        except ImportError:
+            continue
+        patch(mod, "_apply_expansion", seam)
+        patch(mod, "estimate_spectral_norm", norm)
+        patch(mod, "sample_projection", proj)
+    patch(csemb_module, "estimate_spectral_norm", norm)
+    patch(csemb_module, "sample_projection", proj)
+
+    def uninstall():
+        for mod, name, fn in reversed(saved):
+            setattr(mod, name, fn)
+
+    return uninstall

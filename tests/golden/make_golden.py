@@ -1,0 +1,311 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE.
+
+This script is the only place that imports the reference package (`csemb`,
+read-only at /root/reference/pkg/src). It runs in the build container, where
+the reference is importable, and writes small .npz fixtures that travel with
+the repo; nothing on the GPU box reads /root/reference.
+
+    python tests/golden/make_golden.py          # rewrites tests/golden/*.npz
+
+Every fixture records the reference call that produced it (see `CASES` below
+and the `meta` string inside each file).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import logging
+import os
+import re
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+REF_TESTS = "/root/reference/pkg/tests"
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, REF_TESTS)
+sys.dont_write_bytecode = True
+
+import csemb as cs  # noqa: E402  (reference, read-only)
+from csemb import engine as ref_engine  # noqa: E402
+from helpers import random_symmetric, sbm  # noqa: E402  (reference test helpers)
+
+
+class _StepLog(logging.Handler):
+    """Collect the reference's per-step debug records (engine.py:218-220)."""
+
+    pat = re.compile(r"stage=(\d+) cols=(\d+)\+(\d+) r=(\d+) max_abs=(\S+)")
+
+    def __init__(self):
+        super().__init__(logging.DEBUG)
+        self.rows = []
+
+    def emit(self, record):
+        m = self.pat.match(record.getMessage())
+        if m:
+            st, c0, w, r, peak = m.groups()
+            self.rows.append((int(st), int(c0), int(w), int(r), float(peak)))
+
+
+def _capture():
+    h = _StepLog()
+    lg = logging.getLogger("csemb.engine")
+    lg.setLevel(logging.DEBUG)
+    lg.addHandler(h)
+    return h, lg
+
+
+def _csr(S):
+    return dict(
+        n_rows=np.int64(S.n_rows),
+        n_cols=np.int64(S.n_cols),
+        row_offsets=np.asarray(S.row_offsets, dtype=np.int64),
+        col_indices=np.asarray(S.col_indices, dtype=np.int32),
+        values=np.asarray(S.values, dtype=np.float64),
+    )
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _save(name, meta, **arrays):
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, meta=np.array(json.dumps(meta, sort_keys=True)), **arrays)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+class CutAbove:
+    """f(x) = x * 1{x >= c} (config 4's PCA-like weight); a plain callable with
+    breakpoints, used identically by both sides."""
+
+    def __init__(self, c):
+        self.c = float(c)
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return np.where(x >= self.c, x, 0.0)
+
+    def breakpoints(self):
+        return (self.c,)
+
+
+def gen_omega():
+    cases = [(3, 4, 42), (50, 9, 3), (40, 7, 11), (40, 80, 0), (2000, 40, 0), (1000, 96, 123456789)]
+    arrays = {}
+    for n, d, seed in cases:
+        om = cs.sample_projection(n, d, seed)
+        arrays[f"signs_{n}_{d}_{seed}"] = np.packbits(om > 0, axis=None)
+    folds = np.array(
+        [cs.fold_seed(s, t) for s, t in [(0, 0x6E6F726D), (13, 0), (2024, 5), (2**63 + 7, 3)]],
+        dtype=np.uint64,
+    )
+    _save(
+        "omega",
+        {"call": "csemb.sample_projection(n,d,seed) > 0, packbits; fold_seed", "cases": cases,
+         "fold_cases": [(0, 0x6E6F726D), (13, 0), (2024, 5), (2**63 + 7, 3)]},
+        folds=folds,
+        **arrays,
+    )
+
+
+def gen_config1():
+    """BASELINE config 1: SBM n=2000, 4 blocks, p_in .05, p_out .005, graph seed 0,
+    d=40 (seed 0), f = 1{x >= 0.9}, L=60, fp64."""
+    edges, labels = sbm(2000, 4, 0.05, 0.005, np.random.default_rng(0))
+    S = cs.normalized_adjacency(edges, 2000)
+    omega = cs.sample_projection(2000, 40, 0)
+    f = cs.indicator_above(0.9)
+    h, lg = _capture()
+    emb = cs.fast_embed_eig(S, f, 60, omega)
+    lg.removeHandler(h)
+    exp = cs.legendre_coefficients(f, 60)
+    steps = np.array([(r, c0, peak) for (_, c0, _, r, peak) in h.rows], dtype=np.float64)
+    pairs = cs.sample_pairs(2000, 10_000, 0)
+    norm_est = cs.estimate_spectral_norm(S, cs.EmbedConfig(L=60, d=40, seed=0))
+    _save(
+        "config1",
+        {
+            "call": "fast_embed_eig(normalized_adjacency(sbm(2000,4,.05,.005,rng0)), indicator_above(0.9), 60, sample_projection(2000,40,0))",
+            "provenance": emb.provenance,
+            "E_sha256": _sha(emb.values),
+            "E_fro": float(np.linalg.norm(emb.values)),
+            "norm_estimate": norm_est,
+        },
+        edges=edges.astype(np.int32),
+        labels=labels.astype(np.int32),
+        coeffs=exp.coeffs,
+        E=emb.values,
+        step_max_abs=steps,
+        pairs=pairs.astype(np.int32),
+        **_csr(S),
+    )
+
+
+def gen_small_cases():
+    """Small engine cases: cascade, general (dilation), worker/column-subset,
+    polynomial exactness, divergence.  Inputs are stored as CSR so the device
+    side needs no generator."""
+    out = {}
+    meta = {}
+
+    # cascade b=2 vs the reference (tests/test_engine.py:201-215 setup)
+    dense = random_symmetric(80, np.random.default_rng(13), spectral_norm=0.98)
+    S = cs.SparseMatrix.from_dense(dense)
+    cfg = cs.EmbedConfig(L=180, d=8, b=2, seed=13)
+    om = cs.sample_projection(80, 8, 13)
+    counter = cs.SpmvCounter()
+    emb = cs.fast_embed_cascaded(S, cs.indicator_above(0.98), cfg, om, counter=counter)
+    for k, v in _csr(S).items():
+        out[f"cascade_{k}"] = v
+    out["cascade_E"] = emb.values
+    meta["cascade"] = {"call": "fast_embed_cascaded(S80, indicator_above(.98), EmbedConfig(L=180,d=8,b=2,seed=13), sample_projection(80,8,13))",
+                       "provenance": emb.provenance}
+
+    # rectangular general path, b=2 (tests/test_engine.py:243-265 setup)
+    rng = np.random.default_rng(18)
+    A = rng.standard_normal((7, 5))
+    A /= np.linalg.norm(A, 2) * 1.02
+    As = cs.SparseMatrix.from_dense(A)
+    cfg = cs.EmbedConfig(L=80, d=9, b=2, seed=18)
+    rows, cols = cs.fast_embed_general(As, cs.indicator_above(0.4), cfg)
+    for k, v in _csr(As).items():
+        out[f"general_{k}"] = v
+    out["general_rows"] = rows.values
+    out["general_cols"] = cols.values
+    meta["general"] = {"call": "fast_embed_general(A7x5, indicator_above(.4), EmbedConfig(L=80,d=9,b=2,seed=18))",
+                       "provenance": rows.provenance}
+
+    # sparse rectangular, b=1, config-4-like weight (odd extension of x*1{x>=.3})
+    rng = np.random.default_rng(44)
+    m, n = 300, 120
+    Ad = rng.random((m, n)) * (rng.random((m, n)) < 0.05)
+    Ad /= np.linalg.norm(Ad, 2) * 1.01
+    As = cs.SparseMatrix.from_dense(Ad)
+    cfg = cs.EmbedConfig(L=120, d=24, b=1, seed=4)
+    rows, cols = cs.fast_embed_general(As, CutAbove(0.3), cfg)
+    for k, v in _csr(As).items():
+        out[f"general2_{k}"] = v
+    out["general2_rows"] = rows.values
+    out["general2_cols"] = cols.values
+    out["general2_dilated_row_offsets"] = np.asarray(cs.dilate(As).row_offsets)
+    out["general2_dilated_col_indices"] = np.asarray(cs.dilate(As).col_indices, dtype=np.int32)
+    out["general2_dilated_values"] = np.asarray(cs.dilate(As).values)
+    meta["general2"] = {"call": "fast_embed_general(A300x120 sparse, CutAbove(0.3), EmbedConfig(L=120,d=24,seed=4))",
+                        "provenance": rows.provenance}
+
+    # column-chunk crossing width, odd d (d=70 crosses two 32-col chunks)
+    dense = random_symmetric(50, np.random.default_rng(10))
+    S = cs.SparseMatrix.from_dense(dense)
+    om = cs.sample_projection(50, 70, 10)
+    h, lg = _capture()
+    emb = cs.fast_embed_eig(S, cs.indicator_above(0.0), 12, om, n_workers=4)
+    lg.removeHandler(h)
+    for k, v in _csr(S).items():
+        out[f"wide_{k}"] = v
+    out["wide_E"] = emb.values
+    out["wide_steps"] = np.array(sorted((r, c0, peak) for (_, c0, _, r, peak) in h.rows), dtype=np.float64)
+    meta["wide"] = {"call": "fast_embed_eig(S50, indicator_above(0), 12, sample_projection(50,70,10), n_workers=4)"}
+
+    # polynomial exactness input (tests/test_engine.py:119-130, seed 0)
+    rng = np.random.default_rng(100)
+    dense = random_symmetric(150, rng, density=0.1, spectral_norm=0.97)
+    coeffs = rng.standard_normal(6)
+    S = cs.SparseMatrix.from_dense(dense)
+    om = cs.sample_projection(150, 10, 0)
+    emb = cs.fast_embed_eig(S, lambda x: np.polynomial.polynomial.polyval(x, coeffs), 5, om)
+    for k, v in _csr(S).items():
+        out[f"poly_{k}"] = v
+    out["poly_monomial"] = coeffs
+    out["poly_E"] = emb.values
+    out["poly_theta"] = cs.legendre_coefficients(lambda x: np.polynomial.polynomial.polyval(x, coeffs), 5).coeffs
+    meta["poly"] = {"call": "fast_embed_eig(S150, polyval(coeffs), 5, sample_projection(150,10,0))"}
+
+    # divergence (tests/test_engine.py:173-177)
+    S = cs.SparseMatrix.from_dense(10.0 * np.eye(4))
+    om = cs.sample_projection(4, 2, 0)
+    try:
+        cs.fast_embed_eig(S, cs.identity(), 250, om)
+        raise SystemExit("reference did not diverge")
+    except cs.DivergenceError as exc:
+        r = int(re.search(r"r=(\d+)", str(exc)).group(1))
+        meta["divergence"] = {"first_bad_r": r, "message": str(exc)}
+    _save("small_cases", meta, **out)
+
+
+def gen_coefficients():
+    specs = {
+        "ind090_60": (cs.indicator_above(0.9), 60),
+        "ind095_180": (cs.indicator_above(0.95), 180),
+        "commute001_180": (cs.commute_time(0.01), 180),
+        "cut030_odd_120": (cs.odd_extension(CutAbove(0.3)), 120),
+        "ind098_root2_90": (cs.root_function(cs.indicator_above(0.98), 2), 90),
+        "ind040_odd_root2_40": (cs.odd_extension(cs.root_function(cs.indicator_above(0.4), 2)), 40),
+        "identity_1": (cs.identity(), 1),
+        "identity_7": (cs.identity(), 7),
+        "const25_0": (cs.constant(2.5), 0),
+        "table_33": (cs.tabulated([-1.0, -0.2, 0.5, 1.0], [0.0, 1.0, -0.5, 2.0]), 33),
+        "ind09_odd_60": (cs.odd_extension(cs.indicator_above(0.9)), 60),
+        "commute_root3_30": (cs.root_function(cs.commute_time(0.05), 3), 30),
+    }
+    arrays, meta = {}, {}
+    for name, (f, order) in specs.items():
+        e = cs.legendre_coefficients(f, order)
+        arrays[name] = e.coeffs
+        meta[name] = {"describe": getattr(f, "describe", lambda: "callable")(), "sha256": e.digest()}
+    _save("coefficients", meta, **arrays)
+
+
+def gen_norm():
+    arrays, meta = {}, {}
+    cases = {}
+    cases["identity10"] = (cs.SparseMatrix.identity(10), cs.EmbedConfig(L=1, d=1, seed=0))
+    dense = np.zeros((50, 50))
+    dense[0, 0], dense[1, 1] = 0.3, -0.9
+    cases["paddiag"] = (cs.SparseMatrix.from_dense(dense), cs.EmbedConfig(L=1, d=1, seed=1))
+    for seed in range(3):
+        dense = random_symmetric(60, np.random.default_rng(seed), spectral_norm=None)
+        cases[f"rand60_{seed}"] = (cs.SparseMatrix.from_dense(dense), cs.EmbedConfig(L=1, d=1, seed=seed))
+    rng = np.random.default_rng(7)
+    A = rng.random((90, 40)) * (rng.random((90, 40)) < 0.1)
+    cases["dilated90x40_30it"] = (cs.dilate(cs.SparseMatrix.from_dense(A)), cs.EmbedConfig(L=1, d=1, seed=3, norm_iters=30))
+    for name, (S, cfg) in cases.items():
+        est = cs.estimate_spectral_norm(S, cfg)
+        for k, v in _csr(S).items():
+            arrays[f"{name}_{k}"] = v
+        meta[name] = {"estimate": est, "seed": cfg.seed, "norm_iters": cfg.norm_iters,
+                      "norm_vectors_factor": cfg.norm_vectors_factor, "norm_safety": cfg.norm_safety,
+                      "exact_norm": float(np.linalg.norm(S.to_dense(), 2))}
+    _save("norm", meta, **arrays)
+
+
+def gen_builders():
+    arrays, meta = {}, {}
+    rng = np.random.default_rng(5)
+    for i, (n, m) in enumerate([(2, 1), (3, 4), (30, 120), (500, 3000)]):
+        edges = rng.integers(0, n, size=(m, 2))
+        S = cs.normalized_adjacency(edges, n)
+        arrays[f"adj{i}_edges"] = edges.astype(np.int64)
+        for k, v in _csr(S).items():
+            arrays[f"adj{i}_{k}"] = v
+        meta[f"adj{i}"] = {"n": n}
+    A = cs.SparseMatrix.from_dense(np.random.default_rng(6).random((6, 9)) * (np.random.default_rng(7).random((6, 9)) < 0.4))
+    D = cs.dilate(A)
+    for k, v in _csr(A).items():
+        arrays[f"dil_A_{k}"] = v
+    for k, v in _csr(D).items():
+        arrays[f"dil_S_{k}"] = v
+    _save("builders", meta, **arrays)
+
+
+if __name__ == "__main__":
+    gen_omega()
+    gen_config1()
+    gen_small_cases()
+    gen_coefficients()
+    gen_norm()
+    gen_builders()

@@ -1,0 +1,315 @@
+"""Device path vs the oracle / the reference's golden vectors (B200 only).
+
+fp64 is bit-identical to the reference (strict separately-rounded multiply/add
+in stored-entry order); fp32 meets the north_star tolerances: relative
+Frobenius error <= 1e-4 vs the fp64 reference and pairwise cosine error
+<= 1e-4 on 10^4 sampled row pairs.
+"""
+
+import hashlib
+import logging
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1509_08360_b200 as pb
+from conftest import csr_from, load_golden, sparse_from
+from paper_1509_08360_b200 import graphs
+
+pytestmark = pytest.mark.gpu
+
+FP32_REL = 1e-4      # north_star: relative Frobenius error in fp32
+COS_TOL = 1e-4       # north_star: pairwise cosine error on sampled pairs
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(autouse=True)
+def _lib_ready(gpu_lib):
+    yield
+
+
+# --------------------------------------------------------------------------
+# config 1 (BASELINE configs[0]) against the reference's own output
+# --------------------------------------------------------------------------
+class TestConfig1:
+    def test_fp64_bit_exact_given_omega(self, config1):
+        z, meta = config1
+        S = sparse_from(z)
+        emb = pb.fast_embed_eig(S, pb.indicator_above(0.9), 60, O.sample_projection(2000, 40, 0))
+        assert sha(emb.values) == meta["E_sha256"]
+        assert emb.provenance == meta["provenance"]
+
+    def test_fp64_bit_exact_device_omega(self, config1):
+        z, meta = config1
+        S = sparse_from(z)
+        emb = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), pb.EmbedConfig(L=60, d=40, seed=0))
+        assert sha(emb.values) == meta["E_sha256"]
+        assert emb.provenance["spmv_products"] == 60
+        assert emb.provenance["coeffs_sha256"] == meta["provenance"]["coeffs_sha256"]
+
+    def test_step_log_matches_reference(self, config1, caplog):
+        z, _ = config1
+        S = sparse_from(z)
+        with caplog.at_level(logging.DEBUG, logger="csemb.engine"):
+            pb.fast_embed_eig(S, pb.indicator_above(0.9), 60, O.sample_projection(2000, 40, 0))
+        recs = [r.getMessage() for r in caplog.records if r.getMessage().startswith("stage=")]
+        assert len(recs) == 120
+        ref = z["step_max_abs"]
+        got = np.array([float(m.split("max_abs=")[1]) for m in recs])
+        np.testing.assert_allclose(got, ref[:, 2], rtol=1e-12)
+        assert recs[0].startswith("stage=1 cols=0+32 r=1 ") and recs[60].startswith("stage=1 cols=32+8 r=1 ")
+
+    def test_fp32_tolerances(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        om = O.sample_projection(2000, 40, 0)
+        e32 = pb.fast_embed_eig(S, pb.indicator_above(0.9), 60, om, dtype="float32").values
+        assert e32.dtype == np.float64
+        assert rel(e32, z["E"]) <= FP32_REL
+        pairs = z["pairs"]
+        err = np.abs(O.pair_cosines(e32, pairs) - O.pair_cosines(z["E"], pairs)).max()
+        assert err <= COS_TOL
+
+    def test_row_normalised_output(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        om = O.sample_projection(2000, 40, 0)
+        for dt, tol in (("float64", 1e-13), ("float32", FP32_REL)):
+            got = pb.fast_embed_eig(S, pb.indicator_above(0.9), 60, om, dtype=dt, normalize_rows=True).values
+            ref = O.row_normalize(z["E"])
+            assert np.abs(got - ref).max() <= tol
+            pairs = z["pairs"]
+            cos_dev = np.einsum("ij,ij->i", got[pairs[:, 0]], got[pairs[:, 1]])
+            assert np.abs(cos_dev - O.pair_cosines(z["E"], pairs)).max() <= COS_TOL
+
+    def test_repeatable(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        a = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), pb.EmbedConfig(L=60, d=40)).values
+        b = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), pb.EmbedConfig(L=60, d=40)).values
+        assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------
+# engine cases from the reference's suite (golden outputs)
+# --------------------------------------------------------------------------
+class TestEngineCases:
+    def test_cascade_b2(self, small_cases):
+        z, meta = small_cases
+        S = sparse_from(z, "cascade_")
+        counter = pb.SpmvCounter()
+        emb = pb.fast_embed_cascaded(S, pb.indicator_above(0.98), pb.EmbedConfig(L=180, d=8, b=2, seed=13),
+                                     O.sample_projection(80, 8, 13), counter=counter)
+        assert np.array_equal(emb.values, z["cascade_E"])
+        assert counter.products == 180
+        assert emb.provenance == meta["cascade"]["provenance"]
+
+    def test_general_b2(self, small_cases):
+        z, meta = small_cases
+        A = sparse_from(z, "general_")
+        rows, cols = pb.fast_embed_general(A, pb.indicator_above(0.4), pb.EmbedConfig(L=80, d=9, b=2, seed=18))
+        assert np.array_equal(rows.values, z["general_rows"])
+        assert np.array_equal(cols.values, z["general_cols"])
+        assert rows.provenance == meta["general"]["provenance"]
+
+    def test_general_sparse_config4_weight(self, small_cases):
+        z, _ = small_cases
+
+        class CutAbove:
+            def __call__(self, x):
+                x = np.asarray(x, dtype=np.float64)
+                return np.where(x >= 0.3, x, 0.0)
+
+            def breakpoints(self):
+                return (0.3,)
+
+        A = sparse_from(z, "general2_")
+        rows, cols = pb.fast_embed_general(A, CutAbove(), pb.EmbedConfig(L=120, d=24, seed=4))
+        assert np.array_equal(rows.values, z["general2_rows"])
+        assert np.array_equal(cols.values, z["general2_cols"])
+        r32, c32 = pb.fast_embed_general(A, CutAbove(), pb.EmbedConfig(L=120, d=24, seed=4), dtype="float32")
+        assert rel(r32.values, z["general2_rows"]) <= FP32_REL
+
+    def test_chunk_crossing_and_logs(self, small_cases, caplog):
+        z, _ = small_cases
+        S = sparse_from(z, "wide_")
+        om = O.sample_projection(50, 70, 10)
+        with caplog.at_level(logging.DEBUG, logger="csemb.engine"):
+            emb = pb.fast_embed_eig(S, pb.indicator_above(0.0), 12, om, n_workers=4)
+        assert np.array_equal(emb.values, z["wide_E"])
+        got = sorted((int(m.split(" r=")[1].split()[0]), int(m.split("cols=")[1].split("+")[0]),
+                      float(m.split("max_abs=")[1])) for m in (r.getMessage() for r in caplog.records)
+                     if m.startswith("stage="))
+        ref = z["wide_steps"]
+        assert len(got) == len(ref)
+        np.testing.assert_allclose(np.array(got)[:, 2], ref[:, 2], rtol=1e-12)
+
+    def test_polynomial_exactness(self, small_cases):
+        z, _ = small_cases
+        S = sparse_from(z, "poly_")
+        coeffs = z["poly_monomial"]
+        emb = pb.fast_embed_eig(S, lambda x: np.polynomial.polynomial.polyval(x, coeffs), 5,
+                                O.sample_projection(150, 10, 0))
+        assert np.array_equal(emb.values, z["poly_E"])
+
+    def test_column_subset_bit_exact(self, small_cases):
+        z, _ = small_cases
+        S = sparse_from(z, "wide_")
+        om = O.sample_projection(50, 70, 10)
+        full = pb.fast_embed_eig(S, pb.indicator_above(0.1), 15, om).values
+        part = pb.fast_embed_eig(S, pb.indicator_above(0.1), 15, om[:, 30:37]).values
+        assert np.array_equal(part, full[:, 30:37])
+
+    def test_divergence(self, small_cases):
+        _, meta = small_cases
+        S = pb.SparseMatrix.from_dense(10.0 * np.eye(4))
+        with pytest.raises(pb.DivergenceError, match=f"r={meta['divergence']['first_bad_r']} "):
+            pb.fast_embed_eig(S, pb.identity(), 250, O.sample_projection(4, 2, 0))
+
+    def test_order_zero(self):
+        S = pb.SparseMatrix.from_dense(np.diag([0.5, -0.2, 0.1]))
+        om = O.sample_projection(3, 3, 7)
+        emb = pb.fast_embed_eig(S, pb.constant(2.5), 0, om)
+        assert np.array_equal(emb.values, 2.5 * om) and emb.provenance["spmv_products"] == 0
+
+    def test_identity_and_square(self):  # tests/test_engine.py:100-109
+        om = O.sample_projection(8, 4, 5)
+        assert np.allclose(pb.fast_embed_eig(pb.SparseMatrix.identity(8), pb.identity(), 1, om).values, om,
+                           atol=1e-15)
+        S = pb.SparseMatrix.from_dense(np.diag([0.5, -0.5]))
+        om = O.sample_projection(2, 6, 6)
+        assert np.allclose(pb.fast_embed_eig(S, lambda x: x**2, 2, om).values, 0.25 * om, atol=1e-14)
+
+    def test_errors(self):
+        with pytest.raises(ValueError):
+            pb.fast_embed_eig(pb.SparseMatrix.identity(4), pb.identity(), 1, np.zeros((3, 2)))
+        with pytest.raises(ValueError):
+            pb.fast_embed_eig(pb.SparseMatrix.zeros(3, 4), pb.identity(), 1, np.zeros((3, 2)))
+        with pytest.raises(ValueError):
+            pb.fast_embed_eig(pb.SparseMatrix.identity(4), pb.legendre_coefficients(pb.identity(), 3), 2,
+                              np.zeros((4, 2)))
+
+
+# --------------------------------------------------------------------------
+# edge cases and larger inputs against the oracle
+# --------------------------------------------------------------------------
+def _oracle_embed(S, coeffs, om):
+    out, _, bad = O.run_stage(O.CSR.of(S), coeffs, om)
+    assert bad == 0
+    return out
+
+
+class TestEdgeCases:
+    def test_empty_matrix(self):
+        S = pb.SparseMatrix.zeros(6, 6)
+        om = O.sample_projection(6, 5, 1)
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), 10).coeffs
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 10, om).values
+        assert np.array_equal(got, _oracle_embed(S, th, om))
+
+    def test_isolated_vertices_and_zero_rows(self):
+        S = pb.normalized_adjacency([(0, 1), (1, 2), (5, 6)], 9)  # 3, 4, 7, 8 isolated
+        om = O.sample_projection(9, 6, 2)
+        th = pb.legendre_coefficients(pb.indicator_above(0.2), 20).coeffs
+        ref = _oracle_embed(S, th, om)
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 20, om).values
+        assert np.array_equal(got, ref)
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 20, om, normalize_rows=True).values
+        assert np.abs(got - O.row_normalize(ref)).max() <= 1e-15
+        assert np.all(np.linalg.norm(got, axis=1)[[3, 4, 7, 8]] > 0)  # Omega rows survive theta_0
+
+    @pytest.mark.parametrize("d", [1, 2, 3, 5, 7, 8, 9, 31, 33, 64, 65, 97, 130, 300, 517])
+    def test_widths(self, d):
+        S = graphs.sbm(700, 5, 8.0, 2.0, seed=d)
+        om = O.sample_projection(700, d, d)
+        th = pb.legendre_coefficients(pb.indicator_above(0.6), 9).coeffs
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 9, om).values
+        assert np.array_equal(got, _oracle_embed(S, th, om))
+        g32 = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 9, om, dtype="float32").values
+        assert rel(g32, got) <= FP32_REL
+
+    def test_heavy_rows(self):
+        # a star plus a random graph: one row with ~all columns, many with few
+        n = 5000
+        rng = np.random.default_rng(3)
+        e = np.concatenate([np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1),
+                            rng.integers(0, n, size=(20000, 2))])
+        S = pb.normalized_adjacency(e, n)
+        om = O.sample_projection(n, 40, 3)
+        th = pb.legendre_coefficients(pb.commute_time(0.01), 25).coeffs
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 25, om).values
+        assert np.array_equal(got, _oracle_embed(S, th, om))
+
+    def test_midsize_sbm_fp64_fp32(self):
+        S = graphs.sbm(30000, 10, 15.0, 5.0, seed=7)
+        om = O.sample_projection(30000, 80, 7)
+        th = pb.legendre_coefficients(pb.indicator_above(0.95), 40).coeffs
+        ref = _oracle_embed(S, th, om)
+        got = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 40, om).values
+        assert np.array_equal(got, ref)
+        g32 = pb.fast_embed_eig(S, pb.LegendreExpansion(th), 40, om, dtype="float32").values
+        assert rel(g32, ref) <= FP32_REL
+        pairs = O.sample_pairs(30000, 10_000, 1)
+        assert np.abs(O.pair_cosines(g32, pairs) - O.pair_cosines(ref, pairs)).max() <= COS_TOL
+
+
+# --------------------------------------------------------------------------
+# projection block, norm estimate, scaling
+# --------------------------------------------------------------------------
+class TestProjectionAndNorm:
+    def test_projection_golden(self):
+        z, meta = load_golden("omega")
+        for n, d, seed in meta["cases"]:
+            om = pb.sample_projection(n, d, seed)
+            assert np.array_equal(np.packbits(om > 0), z[f"signs_{n}_{d}_{seed}"])
+            assert np.array_equal(om, O.sample_projection(n, d, seed))
+        full = pb.sample_projection(300, 80, 9)
+        assert np.array_equal(pb.sample_projection(300, 80, 9, col0=20, w=17), full[:, 20:37])
+
+    def test_philox_projection(self):
+        n, d = 100_000, 64
+        om = pb.sample_projection(n, d, 0, kind="philox")
+        assert np.all(np.abs(om) == 1.0 / 8.0)
+        assert abs(om.mean()) <= 4.0 * (1 / 8.0) / np.sqrt(n * d)
+        assert not np.array_equal(om, pb.sample_projection(n, d, 0))
+
+    def test_norm_golden(self):
+        z, meta = load_golden("norm")
+        for name, m in meta.items():
+            S = sparse_from(z, name + "_")
+            cfg = pb.EmbedConfig(L=1, d=1, seed=m["seed"], norm_iters=m["norm_iters"])
+            est = pb.estimate_spectral_norm(S, cfg)
+            assert est == pytest.approx(m["estimate"], rel=1e-12, abs=1e-15), name
+            assert est <= 1.01 * m["exact_norm"] + 1e-12
+
+    def test_norm_edge_cases(self):
+        assert pb.estimate_spectral_norm(pb.SparseMatrix.zeros(5, 5), pb.EmbedConfig(L=1, d=1)) == 0.0
+        assert pb.estimate_spectral_norm(pb.SparseMatrix.identity(10), pb.EmbedConfig(L=1, d=1)) == \
+            pytest.approx(1.01, abs=1e-12)
+        with pytest.raises(ValueError):
+            pb.estimate_spectral_norm(pb.SparseMatrix.zeros(3, 4), pb.EmbedConfig(L=1, d=1))
+
+    def test_norm_config1_and_philox_start(self, config1):
+        z, meta = config1
+        S = sparse_from(z)
+        cfg = pb.EmbedConfig(L=60, d=40, seed=0)
+        assert pb.estimate_spectral_norm(S, cfg) == pytest.approx(meta["norm_estimate"], rel=1e-12)
+        est = pb.estimate_spectral_norm(S, cfg, start="philox")
+        assert 0.99 <= est <= 1.01 + 1e-12  # ||S|| = 1 for a normalized adjacency
+
+    def test_matrix_scale_bit_exact(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        dm = pb.DeviceMatrix(S, "float64")
+        f = 1.0 / 1.0099999155519637
+        dm.scale(f)
+        assert np.array_equal(dm.download_values(), S.values * f)
+        dm.close()
