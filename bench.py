@@ -280,7 +280,7 @@ def run_e2e(args, S, coeffs, units, device):
     from paper_1509_08360_b200 import _lib
 
     n, d = S.n_rows, args.d
-    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    pin = lambda a: torch.from_numpy(np.array(a)).pin_memory()  # noqa: E731
     ro, ci, va = pin(S.row_offsets), pin(S.col_indices), pin(S.values)
     block = pin(pb.sample_projection(n, d, 7))
     out = torch.empty((n, d), dtype=torch.float64).pin_memory()

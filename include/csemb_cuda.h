@@ -92,6 +92,17 @@ int csemb_matrix_download_values(csemb_mat *m, double *values_out);
 int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out);
 int csemb_plan_destroy(csemb_plan *p);
 
+/* Plan options.
+ *  CSEMB_OPT_EXACT_PEAKS (default 0): 1 = record the exact per-chunk max|Q(r)|
+ *    of every step (the reference's debug log, engine.py:217-220); 0 = record
+ *    only non-finite flags (+inf key where a chunk diverged), which is all the
+ *    DivergenceError check needs and keeps K1's register footprint small.
+ *  CSEMB_OPT_REVERSE_SWEEP (default 1): alternate the row sweep direction each
+ *    step so the rows written last (still in L2) are gathered first.  */
+#define CSEMB_OPT_EXACT_PEAKS 1
+#define CSEMB_OPT_REVERSE_SWEEP 2
+int csemb_plan_set_option(csemb_plan *p, int option, int64_t value);
+
 /* Device-resident run: _apply_expansion (engine.py:231-258) chained over
  * n_stages cascade stages (engine.py:332-336).  coeffs[0..order] are the
  * stage's Legendre coefficients (LegendreExpansion.coeffs).  The projection

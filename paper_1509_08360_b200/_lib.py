@@ -16,11 +16,12 @@ import numpy as np
 from .errors import CudaUnavailableError, DivergenceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcsemb_cuda.so")
+LIB_PATH = os.environ.get("CSEMB_LIB_PATH") or os.path.join(_HERE, "libcsemb_cuda.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_DIVERGED, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 OMEGA_GIVEN, OMEGA_SPLITMIX, OMEGA_PHILOX = 0, 1, 2
+OPT_EXACT_PEAKS, OPT_REVERSE_SWEEP = 1, 2
 
 DIVERGENCE_MESSAGE = (
     "iteration r={r} produced non-finite values; the matrix likely has "
@@ -56,6 +57,7 @@ SIGNATURES = {
     "csemb_matrix_download_values": (_int, [_p, _p]),
     "csemb_plan_create": (_int, [_p, _i64, _pp]),
     "csemb_plan_destroy": (_int, [_p]),
+    "csemb_plan_set_option": (_int, [_p, _int, _i64]),
     "csemb_plan_run": (_int, [_p, _p, _int, _int, _p, _int, _u64, _i64, _i64, _int]),
     "csemb_plan_download": (_int, [_p, _p, _int]),
     "csemb_plan_output": (_int, [_p, _pp, _pi64, _pi]),

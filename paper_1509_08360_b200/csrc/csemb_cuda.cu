@@ -79,6 +79,9 @@ struct csemb_plan {
     int64_t n_chunks = 0;
     int step_launches = 0;
     bool ran = false;
+    // options (csemb_plan_set_option)
+    int exact_peaks = 0;
+    int reverse_sweep = 1;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -99,9 +102,9 @@ static int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 
 static std::mutex g_occ_mu;
 static std::unordered_map<const void *, int> g_occ;
 
-template <typename T, int G, int VPL, int MODE>
+template <typename T, int G, int VPL, int MODE, int PEAK>
 static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
-    const void *fn = (const void *)k_step<T, G, VPL, MODE>;
+    const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK>;
     const int threads = 256;
     const int W = Vec<T>::W;
     const int nch = ((P.col0 + (P.v0 + P.nvt) * W - 1) >> 5) - ((P.col0 + P.v0 * W) >> 5) + 1;
@@ -119,45 +122,49 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
         per_sm = it->second;
     }
     const int grid = grid_for(P.n_rows * G, threads, sm_count, per_sm);
-    k_step<T, G, VPL, MODE><<<grid, threads, smem, s>>>(P);
+    k_step<T, G, VPL, MODE, PEAK><<<grid, threads, smem, s>>>(P);
     return cudaGetLastError();
 }
 
-template <typename T, int G, int MODE>
+// VPL instantiations: 1..3 for G == 1, 2..3 for wider groups (more vectors per
+// lane spill at the 64-register cap that gives 4 CTAs / 32 warps per SM)
+template <typename T, int G, int MODE, int PEAK>
 static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, int sm) {
-    if (G == 1) {
-        switch (vpl) {
-            case 1: return run_step<T, G, 1, MODE>(P, s, sm);
-            case 2: return run_step<T, G, 2, MODE>(P, s, sm);
-            case 3: return run_step<T, G, 3, MODE>(P, s, sm);
-            default: break;
-        }
+    if constexpr (G == 1) {
+        if (vpl == 1) return run_step<T, G, 1, MODE, PEAK>(P, s, sm);
     }
     switch (vpl) {
-        case 4: return run_step<T, G, 4, MODE>(P, s, sm);
-        case 5: return run_step<T, G, 5, MODE>(P, s, sm);
-        case 6: return run_step<T, G, 6, MODE>(P, s, sm);
-        case 7: return run_step<T, G, 7, MODE>(P, s, sm);
-        case 8: return run_step<T, G, 8, MODE>(P, s, sm);
+        case 2: return run_step<T, G, 2, MODE, PEAK>(P, s, sm);
+        case 3: return run_step<T, G, 3, MODE, PEAK>(P, s, sm);
         default: return cudaErrorInvalidValue;
     }
 }
 
-// G = largest power of two <= nv/4 (>= 1, <= 32), so VPL = ceil(nv/G) in [4, 8]
-// for nv >= 8 and = nv below; a launch covers at most 256 vectors.
+// Target vectors per lane (CSEMB_TARGET_VPL in [2, 3], default 3); the group is
+// the smallest power of two G with ceil(nv/G) <= target, and one launch covers
+// at most 32*target vectors (wider rows are split into column tiles).
+static int target_vpl() {
+    static int t = [] {
+        const char *e = getenv("CSEMB_TARGET_VPL");
+        int v = e ? atoi(e) : 3;
+        return std::min(3, std::max(2, v));
+    }();
+    return t;
+}
+
 static int choose_group(int nv) {
-    int q = std::max(1, nv / 4);
+    const int tv = target_vpl();
     int g = 1;
-    while (g * 2 <= q && g < 32) g *= 2;
+    while (g < 32 && (nv + g - 1) / g > tv) g *= 2;
     return g;
 }
 
-static const int MAX_TILE_VECS = 256;
+static int max_tile_vecs() { return 32 * target_vpl(); }
 
-template <typename T, int MODE>
+template <typename T, int MODE, int PEAK>
 static cudaError_t launch_step(StepParams P, cudaStream_t s, int sm) {
     const int nv_total = P.nvt;
-    const int ntiles = (nv_total + MAX_TILE_VECS - 1) / MAX_TILE_VECS;
+    const int ntiles = (nv_total + max_tile_vecs() - 1) / max_tile_vecs();
     const int base = P.v0;
     for (int t = 0; t < ntiles; ++t) {
         const int lo = (int)((int64_t)nv_total * t / ntiles), hi = (int)((int64_t)nv_total * (t + 1) / ntiles);
@@ -167,19 +174,19 @@ static cudaError_t launch_step(StepParams P, cudaStream_t s, int sm) {
         const int vpl = (P.nvt + G - 1) / G;
         cudaError_t e;
         switch (G) {
-            case 1: e = dispatch_vpl<T, 1, MODE>(vpl, P, s, sm); break;
-            case 2: e = dispatch_vpl<T, 2, MODE>(vpl, P, s, sm); break;
-            case 4: e = dispatch_vpl<T, 4, MODE>(vpl, P, s, sm); break;
-            case 8: e = dispatch_vpl<T, 8, MODE>(vpl, P, s, sm); break;
-            case 16: e = dispatch_vpl<T, 16, MODE>(vpl, P, s, sm); break;
-            default: e = dispatch_vpl<T, 32, MODE>(vpl, P, s, sm); break;
+            case 1: e = dispatch_vpl<T, 1, MODE, PEAK>(vpl, P, s, sm); break;
+            case 2: e = dispatch_vpl<T, 2, MODE, PEAK>(vpl, P, s, sm); break;
+            case 4: e = dispatch_vpl<T, 4, MODE, PEAK>(vpl, P, s, sm); break;
+            case 8: e = dispatch_vpl<T, 8, MODE, PEAK>(vpl, P, s, sm); break;
+            case 16: e = dispatch_vpl<T, 16, MODE, PEAK>(vpl, P, s, sm); break;
+            default: e = dispatch_vpl<T, 32, MODE, PEAK>(vpl, P, s, sm); break;
         }
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
 }
 
-static int tiles_for(int nv) { return (nv + MAX_TILE_VECS - 1) / MAX_TILE_VECS; }
+static int tiles_for(int nv) { return (nv + max_tile_vecs() - 1) / max_tile_vecs(); }
 
 // ---------------------------------------------------------------------------
 // misc API
@@ -504,6 +511,16 @@ extern "C" int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out) {
     return CSEMB_OK;
 }
 
+extern "C" int csemb_plan_set_option(csemb_plan *p, int option, int64_t value) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    switch (option) {
+        case CSEMB_OPT_EXACT_PEAKS: p->exact_peaks = value != 0; return CSEMB_OK;
+        case CSEMB_OPT_REVERSE_SWEEP: p->reverse_sweep = value != 0; return CSEMB_OK;
+        default: return fail(CSEMB_ERR_INVALID, "unknown plan option %d", option);
+    }
+}
+
 extern "C" int csemb_plan_destroy(csemb_plan *p) {
     if (!p) return CSEMB_OK;
     std::lock_guard<std::mutex> lk(p->m->ctx->mu);
@@ -568,10 +585,15 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
             P.beta = 1.0 - 1.0 / (double)r;   // engine.py:216
             P.theta = coeffs[r];
             P.has_prev = r > 1;
-            P.reverse = (r & 1) == 0;
+            P.reverse = p->reverse_sweep && (r & 1) == 0;
             P.peaks = p->peaks + ((size_t)st * order + (r - 1)) * n_chunks;
             P.col0 = (int)col0;
-            if (n > 0) CK(launch_step<T, MODE_RECUR>(P, s, c->sm_count));
+            if (n > 0) {
+                if (p->exact_peaks)
+                    CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, s, c->sm_count));
+                else
+                    CK(launch_step<T, MODE_RECUR, PEAK_FLAG>(P, s, c->sm_count));
+            }
             p->step_launches += tiles;
         }
         if (st == n_stages - 1) CK(cudaEventRecord(p->ev[2], s));
@@ -862,7 +884,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
         P.ldv = ldv;
         P.v0 = 0;
         P.nvt = ldv;
-        e = launch_step<T, MODE_SPMM>(P, s, c->sm_count);  // W = S V (engine.py:184)
+        e = launch_step<T, MODE_SPMM, PEAK_FLAG>(P, s, c->sm_count);  // W = S V (engine.py:184)
         if (e != cudaSuccess) break;
         // Rayleigh quotients and column norms (engine.py:185-187), then V = W / ||W|| (:191)
         k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, Wm, n, (int)k, ld, partial);

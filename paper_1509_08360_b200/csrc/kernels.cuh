@@ -123,132 +123,291 @@ struct StepParams {
     int col0;          // global column of vector 0 (for chunk ids)
 };
 
+// Per-chunk diagnostics.  PEAK_EXACT keeps, per lane slot, the running max of
+// the |Q| bit patterns (the reference's logged max_abs, engine.py:217-220);
+// PEAK_FLAG keeps one bit per 32-column chunk touched by the lane that is set
+// when a non-finite value appears (all the DivergenceError check needs) and
+// costs one register instead of 2*VPL.
+enum { PEAK_FLAG = 0, PEAK_EXACT = 1 };
+
+__device__ __forceinline__ bool vfinite(double2 q) {
+    return (absbits(q.x) < 0x7FF0000000000000ull) & (absbits(q.y) < 0x7FF0000000000000ull);
+}
+__device__ __forceinline__ bool vfinite(float4 q) {
+    const unsigned m = 0x7F800000u;
+    return ((__float_as_uint(q.x) & 0x7FFFFFFFu) < m) & ((__float_as_uint(q.y) & 0x7FFFFFFFu) < m) &
+           ((__float_as_uint(q.z) & 0x7FFFFFFFu) < m) & ((__float_as_uint(q.w) & 0x7FFFFFFFu) < m);
+}
+
+#ifndef K1_MIN_BLOCKS
+#define K1_MIN_BLOCKS 3
+#endif
+#ifndef K1_ABLATE
+#define K1_ABLATE 0  // timing experiments only (results are wrong when nonzero)
+#endif
+
+// Gathers of Q(r-1) rows.  GATHER_MODE 0: ld.global.nc (L1-allocating, 128-byte
+// line requests); 1: ld.global.nc.L1::no_allocate; 2: ld.global.cg (L2 only).
+#ifndef GATHER_MODE
+#define GATHER_MODE 0
+#endif
+#if GATHER_MODE == 3
+#define GATHER_HINT 1
+#define GATHER_OP "ld.global.nc.L2::cache_hint"
+#elif GATHER_MODE == 1
+#define GATHER_OP "ld.global.nc.L1::no_allocate"
+#elif GATHER_MODE == 2
+#define GATHER_OP "ld.global.cg"
+#else
+#define GATHER_OP "ld.global.nc"
+#endif
+#ifdef GATHER_HINT
+// L2 evict_last policy for gathered rows (streams stay evict-first)
+__device__ __forceinline__ uint64_t gather_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double2 ld_gather(const double2 *p) {
+    double2 v;
+    asm(GATHER_OP ".v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(gather_policy()));
+    return v;
+}
+__device__ __forceinline__ float4 ld_gather(const float4 *p) {
+    float4 v;
+    asm(GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(gather_policy()));
+    return v;
+}
+#else
+__device__ __forceinline__ double2 ld_gather(const double2 *p) {
+    double2 v;
+    asm(GATHER_OP ".v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld_gather(const float4 *p) {
+    float4 v;
+    asm(GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+#endif
+// Predicated gathers (branch-free: a not-taken load neither issues traffic nor
+// splits the unrolled entry loop into separate basic blocks, so the scheduler
+// can keep several entries' gathers in flight).
+__device__ __forceinline__ double2 ld_gather_if(const double2 *p, bool ok) {
+    double2 v = make_double2(0.0, 0.0);
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q " GATHER_OP ".v2.f64 {%0,%1}, [%2];\n}"
+        : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((unsigned)ok));
+    return v;
+}
+__device__ __forceinline__ float4 ld_gather_if(const float4 *p, bool ok) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q " GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(p), "r"((unsigned)ok));
+    return v;
+}
+__device__ __forceinline__ double2 vsel(bool c, double2 a, double2 b) {
+    return make_double2(c ? a.x : b.x, c ? a.y : b.y);
+}
+__device__ __forceinline__ float4 vsel(bool c, float4 a, float4 b) {
+    return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
+}
+
 // K1: one recurrence step (MODE_RECUR) or a plain multi-vector SpMM (MODE_SPMM).
-template <typename T, int G, int VPL, int MODE>
-__global__ void __launch_bounds__(256) k_step(const StepParams P) {
+// A group of G lanes owns a row; lane gl holds the 16-byte vectors gl + k*G
+// (k < VPL) of the row's column tile.  The warp's 32/G rows advance together
+// through batches of G stored entries: lane t of a group loads entry base+t
+// (coalesced), the batch is broadcast with full-warp shuffles (the batch loop
+// is warp-uniform, so there are no divergence checks in it), and every lane
+// issues VPL independent 16-byte gathers per entry, consumed strictly in
+// stored order (bit-exact fp64 accumulation order).  The next batch's entries
+// -- or the next row's first batch -- are loaded while the current batch's
+// gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
+// evict-first so L2 keeps the gathered rows of Q(r-1).
+template <typename T, int G, int VPL, int MODE, int PEAK>
+__global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P) {
     typedef typename Vec<T>::type VT;
     constexpr int W = Vec<T>::W;
+    constexpr int RPW = 32 / G;  // rows per warp
     const int lane = threadIdx.x & 31;
-    const int gl = lane & (G - 1);  // lane within the row group
-    const unsigned gmask = (G == 32) ? 0xFFFFFFFFu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int gl = lane & (G - 1);
+    const int grp = lane / G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * RPW;
 
     const T *__restrict__ vals = (const T *)P.vals;
     const int *__restrict__ cols = P.cols;
-    const VT *__restrict__ ycur = (const VT *)P.ycur;
+    const VT *__restrict__ ycur = (const VT *)P.ycur + P.v0 + gl;
     VT *yout = (VT *)P.yout;
     VT *E = (VT *)P.E;
     const T alpha = (T)P.alpha, beta = (T)P.beta, theta = (T)P.theta;
     const bool has_prev = P.has_prev != 0;
+    const int first_chunk = (P.col0 + P.v0 * W) >> 5;
 
     bool valid[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) valid[k] = (gl + k * G) < P.nvt;
-    unsigned long long pk[VPL];
+    unsigned long long pk[PEAK == PEAK_EXACT ? VPL : 1];
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) pk[k] = 0ull;
+    for (int k = 0; k < (PEAK == PEAK_EXACT ? VPL : 1); ++k) pk[k] = 0ull;
+    unsigned badmask = 0u;
 
-    for (int64_t it = gid; it < P.n_rows; it += ngroups) {
-        const int64_t row = P.reverse ? (P.n_rows - 1 - it) : it;
-        const int64_t beg = __ldg(P.rowptr + row), end = __ldg(P.rowptr + row + 1);
+    auto row_of = [&](int64_t it) { return P.reverse ? (P.n_rows - 1 - it) : it; };
+    // current row's extent and first entry batch, loaded one row ahead
+    int64_t it = warp * RPW + grp;
+    int64_t beg = 0, end = 0;
+    if (it < P.n_rows) {
+        const int64_t r = row_of(it);
+        beg = __ldg(P.rowptr + r);
+        end = __ldg(P.rowptr + r + 1);
+    }
+    int myj = 0;
+    T mya = (T)0;
+    if (beg + gl < end) {
+        myj = __ldcs(cols + beg + gl);
+        mya = __ldcs(vals + beg + gl);
+    }
+
+    for (int64_t wbase = warp * RPW; wbase < P.n_rows; wbase += wstride) {  // warp-uniform
+        const bool active = it < P.n_rows;
+        const int64_t row = row_of(it);
+        const int64_t it2 = it + wstride;
+        int64_t beg2 = 0, end2 = 0;
+        if (it2 < P.n_rows) {
+            const int64_t r2 = row_of(it2);
+            beg2 = __ldg(P.rowptr + r2);
+            end2 = __ldg(P.rowptr + r2 + 1);
+        }
+        const int len = (int)(end - beg);
+        const int nb_mine = (len + G - 1) / G;
+        const int nb = __reduce_max_sync(0xFFFFFFFFu, (unsigned)nb_mine);
+
         VT acc[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) acc[k] = vzero(VT());
 
-        // cooperative index/value fetch: lane t of the group holds entry base+t
-        int myj = 0;
-        T mya = (T)0;
-        if (beg + gl < end) {
-            myj = __ldcs(cols + beg + gl);
-            mya = __ldcs(vals + beg + gl);
-        }
-        for (int64_t base = beg; base < end; base += G) {
-            const int cnt = (int)((end - base) < G ? (end - base) : G);
+        for (int b = 0; b < nb; ++b) {
+            // prefetch the next batch of this row, else the next row's first batch
             int nj = 0;
             T na = (T)0;
-            if (base + G + gl < end) {  // prefetch the next batch
-                nj = __ldcs(cols + base + G + gl);
-                na = __ldcs(vals + base + G + gl);
-            }
-            int t = 0;
-            for (; t + 1 < cnt; t += 2) {
-                const int j0 = __shfl_sync(gmask, myj, t, G);
-                const int j1 = __shfl_sync(gmask, myj, t + 1, G);
-                const T a0 = __shfl_sync(gmask, mya, t, G);
-                const T a1 = __shfl_sync(gmask, mya, t + 1, G);
-                const VT *x0 = ycur + (int64_t)j0 * P.ldv + P.v0 + gl;
-                const VT *x1 = ycur + (int64_t)j1 * P.ldv + P.v0 + gl;
-                VT b0[VPL], b1[VPL];
-#pragma unroll
-                for (int k = 0; k < VPL; ++k) {
-                    if (valid[k]) {
-                        b0[k] = __ldg(x0 + k * G);
-                        b1[k] = __ldg(x1 + k * G);
-                    }
+            if (b + 1 < nb_mine) {
+                if (beg + (b + 1) * G + gl < end) {
+                    nj = __ldcs(cols + beg + (b + 1) * G + gl);
+                    na = __ldcs(vals + beg + (b + 1) * G + gl);
                 }
+            } else if (b + 1 >= nb && beg2 + gl < end2) {
+                nj = __ldcs(cols + beg2 + gl);
+                na = __ldcs(vals + beg2 + gl);
+            }
+            const int cnt = len - b * G;  // entries of this batch for my row (may be <= 0)
+            // branch-free, two entries deep: issue entry t+1's gathers, then consume t
+            VT cur[VPL];
+            {
+                const int j = __shfl_sync(0xFFFFFFFFu, myj, 0, G);
+#if (K1_ABLATE & 2)
+                const VT *x = ycur + row * (int64_t)P.ldv;
+#else
+                const VT *x = ycur + (int64_t)j * P.ldv;
+#endif
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) {
-                    if (valid[k]) {
-                        acc[k] = vmadd(acc[k], a0, b0[k]);  // stored order: t before t+1
-                        acc[k] = vmadd(acc[k], a1, b1[k]);
-                    }
+                for (int k = 0; k < VPL; ++k) cur[k] = ld_gather_if(x + k * G, valid[k] && 0 < cnt);
+            }
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                VT nxt[VPL];
+                if (t + 1 < G) {
+                    const int j = __shfl_sync(0xFFFFFFFFu, myj, t + 1, G);
+#if (K1_ABLATE & 2)
+                    const VT *x = ycur + row * (int64_t)P.ldv;
+#else
+                    const VT *x = ycur + (int64_t)j * P.ldv;
+#endif
+#pragma unroll
+                    for (int k = 0; k < VPL; ++k) nxt[k] = ld_gather_if(x + k * G, valid[k] && t + 1 < cnt);
+                }
+                // a padded step (t >= cnt) has a == 0 and cur == 0: acc + (+0) == acc
+                // exactly, because acc is never -0 (it starts at +0, as scipy's y does)
+                const T a = __shfl_sync(0xFFFFFFFFu, mya, t, G);
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, cur[k]);
+                if (t + 1 < G) {
+#pragma unroll
+                    for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
                 }
             }
-            if (t < cnt) {
-                const int j0 = __shfl_sync(gmask, myj, t, G);
-                const T a0 = __shfl_sync(gmask, mya, t, G);
-                const VT *x0 = ycur + (int64_t)j0 * P.ldv + P.v0 + gl;
-#pragma unroll
-                for (int k = 0; k < VPL; ++k)
-                    if (valid[k]) acc[k] = vmadd(acc[k], a0, __ldg(x0 + k * G));
+            if (b + 1 < nb_mine || b + 1 >= nb) {
+                myj = nj;
+                mya = na;
             }
-            myj = nj;
-            mya = na;
+        }
+        if (nb == 0) {  // every row of the warp is empty: move to the next rows' first batch
+            myj = 0;
+            mya = (T)0;
+            if (beg2 + gl < end2) {
+                myj = __ldcs(cols + beg2 + gl);
+                mya = __ldcs(vals + beg2 + gl);
+            }
         }
 
-        VT *yo = yout + row * (int64_t)P.ldv + P.v0 + gl;
-        if (MODE == MODE_SPMM) {
+        if (active) {
+            VT *yo = yout + row * (int64_t)P.ldv + P.v0 + gl;
+            if (MODE == MODE_SPMM) {
 #pragma unroll
-            for (int k = 0; k < VPL; ++k)
-                if (valid[k]) yo[k * G] = acc[k];
-        } else {
-            VT *er = E + row * (int64_t)P.ldv + P.v0 + gl;
-            VT pv[VPL], ev[VPL];
+                for (int k = 0; k < VPL; ++k)
+                    if (valid[k]) yo[k * G] = acc[k];
+            } else {
+                VT *er = E + row * (int64_t)P.ldv + P.v0 + gl;
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                if (valid[k]) {
-                    pv[k] = has_prev ? ld_stream(yo + k * G) : vzero(VT());
-                    ev[k] = ld_stream(er + k * G);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                if (valid[k]) {
-                    const VT q = vrecur(acc[k], alpha, beta, pv[k], has_prev);
-                    yo[k * G] = q;
-                    st_stream(er + k * G, vaccum(ev[k], theta, q));
-                    const unsigned long long b = vpeak(q);
-                    pk[k] = b > pk[k] ? b : pk[k];
+                for (int k = 0; k < VPL; ++k) {
+                    if (valid[k]) {
+#if (K1_ABLATE & 1)
+                        const VT p = vzero(VT()), e = vzero(VT());
+#else
+                        const VT p = has_prev ? ld_stream(yo + k * G) : vzero(VT());
+                        const VT e = ld_stream(er + k * G);
+#endif
+                        const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
+#if (K1_ABLATE & 4)
+                        if (__double_as_longlong((double)vpeak(q)) == 12345) yo[k * G] = q;
+#else
+                        yo[k * G] = q;
+                        st_stream(er + k * G, vaccum(e, theta, q));
+#endif
+                        if (PEAK == PEAK_EXACT) {
+                            const unsigned long long bq = vpeak(q);
+                            unsigned long long &m = pk[PEAK == PEAK_EXACT ? k : 0];
+                            m = bq > m ? bq : m;
+                        } else if (!vfinite(q)) {
+                            badmask |= 1u << (((P.col0 + (P.v0 + gl + k * G) * W) >> 5) - first_chunk);
+                        }
+                    }
                 }
             }
         }
+        it = it2;
+        beg = beg2;
+        end = end2;
     }
 
     if (MODE == MODE_RECUR && P.peaks) {
         // per-chunk max over the block, then one atomic per chunk per block
         extern __shared__ unsigned long long s_peak[];
-        const int first_chunk = (P.col0 + P.v0 * W) >> 5;
         const int last_chunk = (P.col0 + (P.v0 + P.nvt) * W - 1) >> 5;
         const int nch = last_chunk - first_chunk + 1;
         for (int c = threadIdx.x; c < nch; c += blockDim.x) s_peak[c] = 0ull;
         __syncthreads();
+        if (PEAK == PEAK_EXACT) {
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            if (valid[k] && pk[k]) {
-                const int c = ((P.col0 + (P.v0 + gl + k * G) * W) >> 5) - first_chunk;
-                atomicMax(&s_peak[c], pk[k]);
+            for (int k = 0; k < VPL; ++k) {
+                const unsigned long long v = pk[PEAK == PEAK_EXACT ? k : 0];
+                if (valid[k] && v) {
+                    const int c = ((P.col0 + (P.v0 + gl + k * G) * W) >> 5) - first_chunk;
+                    atomicMax(&s_peak[c], v);
+                }
             }
+        } else {
+            // non-finite marker: the +inf key (every finite |Q| key is below it)
+            for (unsigned m = badmask; m; m &= m - 1) atomicMax(&s_peak[__ffs(m) - 1], 0x7FF0000000000000ull);
         }
         __syncthreads();
         for (int c = threadIdx.x; c < nch; c += blockDim.x)

@@ -231,6 +231,16 @@ class Plan:
         _lib.check(self.lib.csemb_plan_create(dm.handle, self.d, C.byref(h)), "csemb_plan_create")
         self.handle = h
         self.last = None
+        self.exact_peaks = False
+
+    def set_option(self, option: int, value: int) -> None:
+        _lib.check(self.lib.csemb_plan_set_option(self.handle, int(option), int(value)), "csemb_plan_set_option")
+
+    def set_exact_peaks(self, on: bool) -> None:
+        """Record exact per-chunk max|Q(r)| (for the debug log) instead of flags."""
+        if bool(on) != self.exact_peaks:
+            self.set_option(_lib.OPT_EXACT_PEAKS, int(bool(on)))
+            self.exact_peaks = bool(on)
 
     def run(self, coeffs, n_stages: int = 1, *, block_dev: int | None = None, omega_kind: int = _lib.OMEGA_SPLITMIX,
             seed: int = 0, col0: int = 0, d_global: int | None = None, normalize_rows: bool = False) -> None:
@@ -365,9 +375,11 @@ def _run(S, coeffs, n_stages, block, *, dtype, device, normalize_rows, omega_kin
         raise ValueError("the recurrence requires a square (symmetric) matrix")
     dm = device_matrix(S, dtype, device)
     d = block.shape[1] if block is not None else int(d)
-    out = dm.plan(d).apply(coeffs, n_stages, block, omega_kind=omega_kind, seed=seed,
-                           normalize_rows=normalize_rows)
-    _log_steps(dm.plan(d).peaks, d)
+    plan = dm.plan(d)
+    plan.set_exact_peaks(logger.isEnabledFor(logging.DEBUG))
+    out = plan.apply(coeffs, n_stages, block, omega_kind=omega_kind, seed=seed, normalize_rows=normalize_rows)
+    if plan.exact_peaks:
+        _log_steps(plan.peaks, d)
     return out
 
 
