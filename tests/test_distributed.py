@@ -1,0 +1,106 @@
+"""Column-sharded multi-rank path on CPU (gloo, world_size 2).
+
+The per-rank compute is injected (the oracle stands in for the GPU kernel, as
+allowed for tests); what is under test is the host-side distributed logic of
+paper_1509_08360_b200.distributed: shard boundaries, global-d hashing of each
+rank's projection slice, the all-gather assembly, and the max-combination of
+per-chunk diagnostics.  The assembled E must equal the single-process result
+bit-for-bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_1509_08360_b200.distributed import column_shards
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem():
+    rng = np.random.default_rng(3)
+    n = 300
+    dense = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.05)
+    dense = 0.5 * (dense + dense.T)
+    dense /= np.abs(np.linalg.eigvalsh(dense)).max() * 1.05
+    import scipy.sparse as sp
+
+    csr = sp.csr_array(dense)
+    csr.sort_indices()
+    S = O.CSR(n, n, csr.indptr, csr.indices, csr.data)
+    coeffs = np.random.default_rng(4).standard_normal(13) * 0.3
+    return S, coeffs
+
+
+def _local_compute(S, coeffs, d, seed, lo, hi, dtype):
+    """Oracle stand-in for one rank: columns [lo, hi) hashed with the global d,
+    plus per-GLOBAL-chunk peaks (columns are independent, so each chunk slice
+    is run on its own)."""
+    order = len(coeffs) - 1
+    n_chunks = (d + 31) // 32
+    block = O.sample_projection(S.n_rows, d, seed, col0=lo, w=hi - lo)
+    E, _, _ = O.run_stage(S, coeffs, block)
+    peaks = np.zeros((1, order, n_chunks))
+    for ch in range(lo // 32, (hi - 1) // 32 + 1):
+        a, b = max(lo, 32 * ch), min(hi, 32 * ch + 32)
+        _, pk, _ = O.run_stage(S, coeffs, block[:, a - lo:b - lo])
+        peaks[0, :, ch] = pk[:, 0]
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    return torch.from_numpy(E).to(tdt), peaks
+
+
+def _worker(rank, world, port, d, seed, dtype, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import embed_column_sharded
+
+        S, coeffs = _problem()
+        E, peaks = embed_column_sharded(
+            S, coeffs, d, seed=seed, dtype=dtype, normalize_rows=False,
+            compute=lambda lo, hi: _local_compute(S, coeffs, d, seed, lo, hi, dtype))
+        if rank == 0:
+            np.savez(result_path, E=E.numpy().astype(np.float64), peaks=peaks)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,dtype", [(70, "f64"), (80, "f32"), (5, "f64")])
+def test_column_sharded_matches_single_process(tmp_path, d, dtype):
+    world, seed = 2, 11
+    out = str(tmp_path / "r.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), d, seed, dtype, out), nprocs=world,
+                       start_method="spawn", join=True)
+    got = np.load(out)
+    S, coeffs = _problem()
+    ref, ref_peaks, _ = O.run_stage(S, coeffs, O.sample_projection(S.n_rows, d, seed))
+    if dtype == "f64":
+        assert np.array_equal(got["E"], ref)
+    else:
+        assert np.array_equal(got["E"], ref.astype(np.float32).astype(np.float64))
+    np.testing.assert_array_equal(got["peaks"][0], ref_peaks)
+
+
+def test_shard_boundaries():
+    for d in (1, 5, 40, 70, 80, 96, 517):
+        for world in (1, 2, 3, 4, 8):
+            for align in (1, 2, 4):
+                sh = column_shards(d, world, align)
+                assert sh[0][0] == 0 and sh[-1][1] == d and len(sh) == world
+                assert all(a <= b for a, b in sh)
+                assert all(sh[i][1] == sh[i + 1][0] for i in range(world - 1))
+                assert all(lo % align == 0 for lo, _ in sh)
+    assert column_shards(80, 8, 2) == [(i * 10, i * 10 + 10) for i in range(8)]
+    with pytest.raises(ValueError):
+        column_shards(0, 2, 2)
