@@ -140,7 +140,13 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 }
 
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS 3
+#define K1_MIN_BLOCKS 0  // 0: 2 CTAs/SM for fp64 (128 registers), 3 for fp32 (80 registers)
+#endif
+#ifndef K1_DEPTH
+#define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
+#endif
+#ifndef K1_EARLY_EPI
+#define K1_EARLY_EPI 0  // 1: issue the row set's Q(r-2)/E loads at the start of its last batch
 #endif
 #ifndef K1_ABLATE
 #define K1_ABLATE 0  // timing experiments only (results are wrong when nonzero)
@@ -225,7 +231,7 @@ __device__ __forceinline__ float4 vsel(bool c, float4 a, float4 b) {
 // gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
 // evict-first so L2 keeps the gathered rows of Q(r-1).
 template <typename T, int G, int VPL, int MODE, int PEAK>
-__global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : 3))) k_step(const StepParams P) {
     typedef typename Vec<T>::type VT;
     constexpr int W = Vec<T>::W;
     constexpr int RPW = 32 / G;  // rows per warp
@@ -268,6 +274,19 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P)
         mya = __ldcs(vals + beg + gl);
     }
 
+    // gathers of the first D-1 entries of the current batch, carried across batches
+    constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (sizeof(T) == 8 ? 4 : 2);
+    constexpr int D = (DEPTH < G) ? DEPTH : G;
+    static_assert(G % D == 0, "pipeline depth must divide the batch width");
+    VT buf[D][VPL];
+#pragma unroll
+    for (int e = 0; e < D - 1; ++e) {
+        const int j = __shfl_sync(0xFFFFFFFFu, myj, e, G);
+        const VT *x = ycur + (int64_t)j * P.ldv;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) buf[e][k] = ld_gather_if(x + k * G, valid[k] && e < end - beg);
+    }
+
     for (int64_t wbase = warp * RPW; wbase < P.n_rows; wbase += wstride) {  // warp-uniform
         const bool active = it < P.n_rows;
         const int64_t row = row_of(it);
@@ -286,54 +305,68 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P)
 #pragma unroll
         for (int k = 0; k < VPL; ++k) acc[k] = vzero(VT());
 
+        VT *const yo_row = yout + row * (int64_t)P.ldv + P.v0 + gl;
+        VT *const er_row = E + row * (int64_t)P.ldv + P.v0 + gl;
+        VT pv[VPL], ev[VPL];  // this row set's streamed epilogue operands
+#if K1_EARLY_EPI
+        const bool early = MODE == MODE_RECUR;
+#else
+        const bool early = false;
+#endif
         for (int b = 0; b < nb; ++b) {
+            if (early && b == nb - 1) {  // warp-uniform: overlap them with the last batch's gathers
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const bool ok = active && valid[k];
+                    pv[k] = (ok && has_prev) ? ld_stream(yo_row + k * G) : vzero(VT());
+                    ev[k] = ok ? ld_stream(er_row + k * G) : vzero(VT());
+                }
+            }
             // prefetch the next batch of this row, else the next row's first batch
             int nj = 0;
             T na = (T)0;
+            int ncnt = 0;  // entries of that next batch for my row
             if (b + 1 < nb_mine) {
+                ncnt = len - (b + 1) * G;
                 if (beg + (b + 1) * G + gl < end) {
                     nj = __ldcs(cols + beg + (b + 1) * G + gl);
                     na = __ldcs(vals + beg + (b + 1) * G + gl);
                 }
-            } else if (b + 1 >= nb && beg2 + gl < end2) {
-                nj = __ldcs(cols + beg2 + gl);
-                na = __ldcs(vals + beg2 + gl);
+            } else if (b + 1 >= nb) {
+                ncnt = (int)(end2 - beg2);
+                if (beg2 + gl < end2) {
+                    nj = __ldcs(cols + beg2 + gl);
+                    na = __ldcs(vals + beg2 + gl);
+                }
             }
             const int cnt = len - b * G;  // entries of this batch for my row (may be <= 0)
-            // branch-free, two entries deep: issue entry t+1's gathers, then consume t
-            VT cur[VPL];
-            {
-                const int j = __shfl_sync(0xFFFFFFFFu, myj, 0, G);
+            // branch-free pipeline, D entries deep: step t issues the gathers of entry
+            // t+D-1 (spilling into the NEXT batch's first entries near the end, so no
+            // batch or row-set epilogue starts with an empty pipeline) and consumes t
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                const int e = t + D - 1;
+                const int j = (e < G) ? __shfl_sync(0xFFFFFFFFu, myj, e % G, G)
+                                      : __shfl_sync(0xFFFFFFFFu, nj, e % G, G);
+                const bool more = (e < G) ? (e < cnt) : (e - G < ncnt);
 #if (K1_ABLATE & 2)
                 const VT *x = ycur + row * (int64_t)P.ldv;
 #else
                 const VT *x = ycur + (int64_t)j * P.ldv;
 #endif
+                if (D > 1) {
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) cur[k] = ld_gather_if(x + k * G, valid[k] && 0 < cnt);
-            }
-#pragma unroll
-            for (int t = 0; t < G; ++t) {
-                VT nxt[VPL];
-                if (t + 1 < G) {
-                    const int j = __shfl_sync(0xFFFFFFFFu, myj, t + 1, G);
-#if (K1_ABLATE & 2)
-                    const VT *x = ycur + row * (int64_t)P.ldv;
-#else
-                    const VT *x = ycur + (int64_t)j * P.ldv;
-#endif
-#pragma unroll
-                    for (int k = 0; k < VPL; ++k) nxt[k] = ld_gather_if(x + k * G, valid[k] && t + 1 < cnt);
+                    for (int k = 0; k < VPL; ++k) buf[e % D][k] = ld_gather_if(x + k * G, valid[k] && more);
                 }
-                // a padded step (t >= cnt) has a == 0 and cur == 0: acc + (+0) == acc
+                // a padded step (t >= cnt) has a == 0 and a zero vector: acc + (+0) == acc
                 // exactly, because acc is never -0 (it starts at +0, as scipy's y does)
                 const T a = __shfl_sync(0xFFFFFFFFu, mya, t, G);
+                if (D == 1) {
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, cur[k]);
-                if (t + 1 < G) {
-#pragma unroll
-                    for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
+                    for (int k = 0; k < VPL; ++k) buf[0][k] = ld_gather_if(x + k * G, valid[k] && more);
                 }
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, buf[t % D][k]);
             }
             if (b + 1 < nb_mine || b + 1 >= nb) {
                 myj = nj;
@@ -346,6 +379,13 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P)
             if (beg2 + gl < end2) {
                 myj = __ldcs(cols + beg2 + gl);
                 mya = __ldcs(vals + beg2 + gl);
+            }
+#pragma unroll
+            for (int e = 0; e < D - 1; ++e) {
+                const int j = __shfl_sync(0xFFFFFFFFu, myj, e, G);
+                const VT *x = ycur + (int64_t)j * P.ldv;
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) buf[e][k] = ld_gather_if(x + k * G, valid[k] && e < end2 - beg2);
             }
         }
 
@@ -363,8 +403,9 @@ __global__ void __launch_bounds__(256, K1_MIN_BLOCKS) k_step(const StepParams P)
 #if (K1_ABLATE & 1)
                         const VT p = vzero(VT()), e = vzero(VT());
 #else
-                        const VT p = has_prev ? ld_stream(yo + k * G) : vzero(VT());
-                        const VT e = ld_stream(er + k * G);
+                        const bool had = early && nb > 0;
+                        const VT p = had ? pv[k] : (has_prev ? ld_stream(yo + k * G) : vzero(VT()));
+                        const VT e = had ? ev[k] : ld_stream(er + k * G);
 #endif
                         const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
 #if (K1_ABLATE & 4)
