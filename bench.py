@@ -188,9 +188,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             dm.ctx.sync()
             torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1) / args.steps
-        # per-launch K1 time of the last step (events bracket the K1 launches only)
+        # K1 time per recurrence step (events bracket the step launches of the last run)
         _, steps_ms, launches = plan.timing()
-        k1_ms = steps_ms / max(launches, 1)
+        k1_ms = steps_ms / L
         if world > 1:
             t = torch.tensor([ms], device=f"cuda:{local_rank}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

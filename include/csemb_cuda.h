@@ -98,9 +98,17 @@ int csemb_plan_destroy(csemb_plan *p);
  *    only non-finite flags (+inf key where a chunk diverged), which is all the
  *    DivergenceError check needs and keeps K1's register footprint small.
  *  CSEMB_OPT_REVERSE_SWEEP (default 1): alternate the row sweep direction each
- *    step so the rows written last (still in L2) are gathered first.  */
+ *    step so the rows written last (still in L2) are gathered first.
+ *  CSEMB_OPT_SPLIT_THRESHOLD / CSEMB_OPT_ROW_ORDER: load balancing for skewed
+ *    (power-law, dilation) row lengths; rows at or below the threshold keep the
+ *    reference's stored-order accumulation (bit-exact).  */
 #define CSEMB_OPT_EXACT_PEAKS 1
 #define CSEMB_OPT_REVERSE_SWEEP 2
+#define CSEMB_OPT_SPLIT_THRESHOLD 3 /* rows longer than this (default 4096) are split
+                                       into 1024-entry chunks summed in chunk order;
+                                       0 = never split (bit-exact for every input) */
+#define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default), 0 natural, 1 bucketed by
+                                       batch count (skewed row lengths) */
 int csemb_plan_set_option(csemb_plan *p, int option, int64_t value);
 
 /* Device-resident run: _apply_expansion (engine.py:231-258) chained over

@@ -56,6 +56,23 @@ struct csemb_ctx {
     std::mutex mu;
 };
 
+// Load-balance schedule of a matrix for one group width G (see K1c in kernels.cuh):
+// rows longer than `threshold` are cut into chunks of `chunk` entries (heavy);
+// the other rows are swept in natural order or, when their lengths are skewed,
+// stably bucketed by batch count ceil(len/G) so a warp's rows need the same
+// number of batches.
+struct Schedule {
+    int G = 0;
+    int64_t threshold = 0;
+    int order = 0;
+    int *perm = nullptr;  // light rows (null: natural order, no heavy rows)
+    int64_t n_light = 0;
+    int64_t *cbeg = nullptr, *cend = nullptr;  // heavy-row chunk entry ranges
+    int64_t n_chunks = 0;
+    int *hrows = nullptr, *hoff = nullptr;     // heavy rows and their chunk offsets
+    int n_heavy = 0;
+};
+
 struct csemb_mat {
     csemb_ctx *ctx = nullptr;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;
@@ -63,6 +80,8 @@ struct csemb_mat {
     int64_t *rowptr = nullptr;
     int *cols = nullptr;
     void *vals = nullptr;
+    std::vector<int64_t> rowptr_host;
+    std::vector<Schedule *> schedules;
 };
 
 struct csemb_plan {
@@ -82,8 +101,22 @@ struct csemb_plan {
     // options (csemb_plan_set_option)
     int exact_peaks = 0;
     int reverse_sweep = 1;
+    int64_t split_threshold = 4096;  // 0: never split rows (bit-exact for every input)
+    int row_order = -1;              // -1 auto, 0 natural, 1 bucketed by batch count
+    void *partials = nullptr;        // heavy-row chunk partial sums
+    size_t partials_bytes = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+
+static void sched_free(Schedule *sc) {
+    if (!sc) return;
+    cudaFree(sc->perm);
+    cudaFree(sc->cbeg);
+    cudaFree(sc->cend);
+    cudaFree(sc->hrows);
+    cudaFree(sc->hoff);
+    delete sc;
+}
 
 static size_t dsize(int dtype) { return dtype == CSEMB_F32 ? 4 : 8; }
 static int vec_w(int dtype) { return dtype == CSEMB_F32 ? 4 : 2; }
@@ -162,10 +195,28 @@ static int choose_group(int nv) {
 static int max_tile_vecs() { return 32 * target_vpl(); }
 
 template <typename T, int MODE, int PEAK>
-static cudaError_t launch_step(StepParams P, cudaStream_t s, int sm) {
+static cudaError_t dispatch_group(int G, int vpl, const StepParams &P, cudaStream_t s, int sm) {
+    switch (G) {
+        case 1: return dispatch_vpl<T, 1, MODE, PEAK>(vpl, P, s, sm);
+        case 2: return dispatch_vpl<T, 2, MODE, PEAK>(vpl, P, s, sm);
+        case 4: return dispatch_vpl<T, 4, MODE, PEAK>(vpl, P, s, sm);
+        case 8: return dispatch_vpl<T, 8, MODE, PEAK>(vpl, P, s, sm);
+        case 16: return dispatch_vpl<T, 16, MODE, PEAK>(vpl, P, s, sm);
+        default: return dispatch_vpl<T, 32, MODE, PEAK>(vpl, P, s, sm);
+    }
+}
+
+// One K1 step over all column tiles, with the load-balance schedule `sc`
+// (may be null): heavy-row chunks (K1 MODE_SPMM into `partials`), the light
+// rows (K1 through the permutation), then the heavy-row combine + epilogue.
+// Returns the number of kernel launches through *launches.
+template <typename T, int MODE, int PEAK>
+static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials, cudaStream_t s, int sm,
+                               int *launches = nullptr) {
     const int nv_total = P.nvt;
     const int ntiles = (nv_total + max_tile_vecs() - 1) / max_tile_vecs();
     const int base = P.v0;
+    int nl = 0;
     for (int t = 0; t < ntiles; ++t) {
         const int lo = (int)((int64_t)nv_total * t / ntiles), hi = (int)((int64_t)nv_total * (t + 1) / ntiles);
         P.v0 = base + lo;
@@ -173,20 +224,125 @@ static cudaError_t launch_step(StepParams P, cudaStream_t s, int sm) {
         const int G = choose_group(P.nvt);
         const int vpl = (P.nvt + G - 1) / G;
         cudaError_t e;
-        switch (G) {
-            case 1: e = dispatch_vpl<T, 1, MODE, PEAK>(vpl, P, s, sm); break;
-            case 2: e = dispatch_vpl<T, 2, MODE, PEAK>(vpl, P, s, sm); break;
-            case 4: e = dispatch_vpl<T, 4, MODE, PEAK>(vpl, P, s, sm); break;
-            case 8: e = dispatch_vpl<T, 8, MODE, PEAK>(vpl, P, s, sm); break;
-            case 16: e = dispatch_vpl<T, 16, MODE, PEAK>(vpl, P, s, sm); break;
-            default: e = dispatch_vpl<T, 32, MODE, PEAK>(vpl, P, s, sm); break;
+        if (sc && sc->n_chunks > 0) {
+            StepParams C = P;
+            C.rbeg = sc->cbeg;
+            C.rend = sc->cend;
+            C.perm = nullptr;
+            C.n_rows = sc->n_chunks;
+            C.yout = partials;
+            C.E = nullptr;
+            C.reverse = 0;
+            C.peaks = nullptr;
+            e = dispatch_group<T, MODE_SPMM, PEAK_FLAG>(G, vpl, C, s, sm);
+            if (e != cudaSuccess) return e;
+            ++nl;
         }
-        if (e != cudaSuccess) return e;
+        StepParams L = P;
+        if (sc && sc->perm) {
+            L.perm = sc->perm;
+            L.n_rows = sc->n_light;
+        }
+        if (L.n_rows > 0) {
+            e = dispatch_group<T, MODE, PEAK>(G, vpl, L, s, sm);
+            if (e != cudaSuccess) return e;
+            ++nl;
+        }
+        if (sc && sc->n_heavy > 0) {
+            HeavyParams H;
+            H.rows = sc->hrows;
+            H.chunk_off = sc->hoff;
+            H.partials = partials;
+            H.n_heavy = sc->n_heavy;
+            const int grid = grid_for((int64_t)sc->n_heavy * 32, 256, sm, 8);
+            k_heavy_combine<T, MODE, PEAK><<<grid, 256, 0, s>>>(P, H);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            ++nl;
+        }
     }
+    if (launches) *launches += nl;
     return cudaSuccess;
 }
 
-static int tiles_for(int nv) { return (nv + max_tile_vecs() - 1) / max_tile_vecs(); }
+static const int64_t HEAVY_CHUNK = 1024;  // entries per chunk of a split heavy row
+
+// Build (or fetch) the schedule of matrix m for group width G.
+static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out) {
+    *out = nullptr;
+    for (Schedule *sc : m->schedules)
+        if (sc->G == G && sc->threshold == threshold && sc->order == order) {
+            *out = sc;
+            return CSEMB_OK;
+        }
+    const std::vector<int64_t> &rp = m->rowptr_host;
+    const int64_t n = m->n_rows;
+    std::vector<int> light, hrows, hoff(1, 0);
+    std::vector<int64_t> cbeg, cend;
+    light.reserve((size_t)n);
+    double sum = 0.0, sum2 = 0.0;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t len = rp[r + 1] - rp[r];
+        if (threshold > 0 && len > threshold) {
+            hrows.push_back((int)r);
+            for (int64_t b = rp[r]; b < rp[r + 1]; b += HEAVY_CHUNK) {
+                cbeg.push_back(b);
+                cend.push_back(std::min(b + HEAVY_CHUNK, rp[r + 1]));
+            }
+            hoff.push_back((int)cbeg.size());
+        } else {
+            light.push_back((int)r);
+            sum += (double)len;
+            sum2 += (double)len * (double)len;
+        }
+    }
+    const double nl = (double)std::max<size_t>(light.size(), 1);
+    const double mean = sum / nl, var = std::max(0.0, sum2 / nl - mean * mean);
+    const bool bucket = order == 1 || (order < 0 && mean > 0 && std::sqrt(var) > 0.5 * mean);
+    if (bucket) {  // stable counting sort of the light rows by batch count
+        const int64_t cap = 1 << 16;
+        std::vector<int64_t> cnt((size_t)cap + 2, 0);
+        auto key = [&](int r) { return std::min<int64_t>((rp[r + 1] - rp[r] + G - 1) / G, cap); };
+        for (int r : light) ++cnt[(size_t)key(r) + 1];
+        for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+        std::vector<int> sorted(light.size());
+        for (int r : light) sorted[(size_t)cnt[(size_t)key(r)]++] = r;
+        light.swap(sorted);
+    }
+    Schedule *sc = new Schedule();
+    sc->G = G;
+    sc->threshold = threshold;
+    sc->order = order;
+    sc->n_light = (int64_t)light.size();
+    sc->n_heavy = (int)hrows.size();
+    sc->n_chunks = (int64_t)cbeg.size();
+    cudaError_t e = cudaSuccess;
+    if (bucket || sc->n_heavy > 0) {
+        e = cudaMalloc(&sc->perm, sizeof(int) * std::max<size_t>(light.size(), 1));
+        if (e == cudaSuccess && !light.empty())
+            e = cudaMemcpy(sc->perm, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && sc->n_heavy > 0) {
+        e = cudaMalloc(&sc->cbeg, 8 * cbeg.size());
+        if (e == cudaSuccess) e = cudaMalloc(&sc->cend, 8 * cend.size());
+        if (e == cudaSuccess) e = cudaMalloc(&sc->hrows, 4 * hrows.size());
+        if (e == cudaSuccess) e = cudaMalloc(&sc->hoff, 4 * hoff.size());
+        if (e == cudaSuccess) e = cudaMemcpy(sc->cbeg, cbeg.data(), 8 * cbeg.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(sc->cend, cend.data(), 8 * cend.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(sc->hrows, hrows.data(), 4 * hrows.size(), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(sc->hoff, hoff.data(), 4 * hoff.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        sched_free(sc);
+        return fail(e == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, "schedule: %s",
+                    cudaGetErrorString(e));
+    }
+    m->schedules.push_back(sc);
+    *out = sc;
+    return CSEMB_OK;
+}
+
 
 // ---------------------------------------------------------------------------
 // misc API
@@ -256,6 +412,7 @@ extern "C" int csemb_ctx_sm_count(csemb_ctx *c, int *out) {
 // ---------------------------------------------------------------------------
 static void mat_free(csemb_mat *m) {
     if (!m) return;
+    for (Schedule *sc : m->schedules) sched_free(sc);
     cudaFree(m->rowptr);
     cudaFree(m->cols);
     cudaFree(m->vals);
@@ -327,6 +484,7 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
     csemb_mat *m = nullptr;
     rc = mat_alloc(c, n_rows, n_cols, nnz, dtype, &m);
     if (rc) return rc;
+    m->rowptr_host.assign(row_offsets, row_offsets + n_rows + 1);
     cudaStream_t s = c->stream;
     cudaError_t e = cudaMemcpyAsync(m->rowptr, row_offsets, sizeof(int64_t) * (size_t)(n_rows + 1),
                                     cudaMemcpyHostToDevice, s);
@@ -406,6 +564,13 @@ extern "C" int csemb_matrix_upload_device(csemb_ctx *c, int64_t n_rows, int64_t 
         mat_free(m);
         return fail(CSEMB_ERR_INVALID, hbad ? "column index out of range" : "row_offsets must run from 0 to nnz");
     }
+    m->rowptr_host.resize((size_t)n_rows + 1);
+    CK(cudaMemcpy(m->rowptr_host.data(), m->rowptr, 8 * ((size_t)n_rows + 1), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n_rows; ++i)
+        if (m->rowptr_host[i + 1] < m->rowptr_host[i]) {
+            mat_free(m);
+            return fail(CSEMB_ERR_INVALID, "row_offsets must be non-decreasing");
+        }
     *out = m;
     return CSEMB_OK;
 }
@@ -475,6 +640,7 @@ static void plan_free(csemb_plan *p) {
     cudaFree(p->E);
     cudaFree(p->staging);
     cudaFree(p->peaks);
+    cudaFree(p->partials);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     delete p;
@@ -517,6 +683,14 @@ extern "C" int csemb_plan_set_option(csemb_plan *p, int option, int64_t value) {
     switch (option) {
         case CSEMB_OPT_EXACT_PEAKS: p->exact_peaks = value != 0; return CSEMB_OK;
         case CSEMB_OPT_REVERSE_SWEEP: p->reverse_sweep = value != 0; return CSEMB_OK;
+        case CSEMB_OPT_SPLIT_THRESHOLD:
+            if (value < 0) return fail(CSEMB_ERR_INVALID, "split threshold must be >= 0");
+            p->split_threshold = value;
+            return CSEMB_OK;
+        case CSEMB_OPT_ROW_ORDER:
+            if (value < -1 || value > 1) return fail(CSEMB_ERR_INVALID, "row order must be -1, 0 or 1");
+            p->row_order = (int)value;
+            return CSEMB_OK;
         default: return fail(CSEMB_ERR_INVALID, "unknown plan option %d", option);
     }
 }
@@ -560,7 +734,21 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
     T *E = (T *)p->E;
     const double scale = 1.0 / std::sqrt((double)d_global);
     const int gi = grid_for(n * (int64_t)ld, 256, c->sm_count, 16);
-    const int tiles = tiles_for(ldv);
+    // load-balance schedule for this width (cached on the matrix)
+    Schedule *sc = nullptr;
+    if (n > 0) {
+        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold,
+                                    p->row_order, &sc);
+        if (rc) return rc;
+        const size_t pbytes = (size_t)sc->n_chunks * (size_t)ld * sizeof(T);
+        if (pbytes > p->partials_bytes) {
+            cudaFree(p->partials);
+            p->partials = nullptr;
+            p->partials_bytes = 0;
+            CK(cudaMalloc(&p->partials, pbytes));
+            p->partials_bytes = pbytes;
+        }
+    }
     CK(cudaEventRecord(p->ev[0], s));
     for (int st = 0; st < n_stages; ++st) {
         const int kind = st > 0 ? OMEGA_FROM_E : omega_kind;
@@ -571,6 +759,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
         if (st == 0) CK(cudaEventRecord(p->ev[1], s));
         for (int r = 1; r <= order; ++r) {
             StepParams P;
+            std::memset(&P, 0, sizeof P);
             P.rowptr = m->rowptr;
             P.cols = m->cols;
             P.vals = m->vals;
@@ -590,11 +779,10 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
             P.col0 = (int)col0;
             if (n > 0) {
                 if (p->exact_peaks)
-                    CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, s, c->sm_count));
+                    CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, sc, p->partials, s, c->sm_count, &p->step_launches));
                 else
-                    CK(launch_step<T, MODE_RECUR, PEAK_FLAG>(P, s, c->sm_count));
+                    CK(launch_step<T, MODE_RECUR, PEAK_FLAG>(P, sc, p->partials, s, c->sm_count, &p->step_launches));
             }
-            p->step_launches += tiles;
         }
         if (st == n_stages - 1) CK(cudaEventRecord(p->ev[2], s));
         // the stage output lives in E; the next stage re-seeds Q(0) from it
@@ -872,6 +1060,16 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
         k_colscale<T><<<gs, 256, 0, s>>>(V, V, inv, n, (int)k, ld);
         e = cudaGetLastError();
     }
+    Schedule *sc = nullptr;
+    void *partials = nullptr;
+    if (e == cudaSuccess) {
+        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), 4096, -1, &sc);
+        if (rc) {
+            cudaFree(V); cudaFree(Wm); cudaFree(stage); cudaFree(partial); cudaFree(rq); cudaFree(inv);
+            return rc;
+        }
+        if (sc->n_chunks) e = cudaMalloc(&partials, (size_t)sc->n_chunks * (size_t)ld * sizeof(T));
+    }
     for (int it = 0; it < iters && e == cudaSuccess; ++it) {
         StepParams P;
         std::memset(&P, 0, sizeof P);
@@ -884,7 +1082,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
         P.ldv = ldv;
         P.v0 = 0;
         P.nvt = ldv;
-        e = launch_step<T, MODE_SPMM, PEAK_FLAG>(P, s, c->sm_count);  // W = S V (engine.py:184)
+        e = launch_step<T, MODE_SPMM, PEAK_FLAG>(P, sc, partials, s, c->sm_count);  // W = S V (engine.py:184)
         if (e != cudaSuccess) break;
         // Rayleigh quotients and column norms (engine.py:185-187), then V = W / ||W|| (:191)
         k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, Wm, n, (int)k, ld, partial);
@@ -900,6 +1098,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     cudaFree(V);
     cudaFree(Wm);
     cudaFree(stage);
+    cudaFree(partials);
     cudaFree(partial);
     cudaFree(rq);
     cudaFree(inv);

@@ -121,6 +121,12 @@ struct StepParams {
     int reverse;       // sweep rows in descending order (L2 reuse of the tail)
     unsigned long long *peaks;  // this step's per-chunk max|Q| keys (MODE_RECUR), or null
     int col0;          // global column of vector 0 (for chunk ids)
+    // load-balance schedule (optional): row i of the sweep is perm[i]; entry
+    // ranges [rbeg[r], rend[r]) replace rowptr (used for the split chunks of
+    // heavy rows, which are written to yout at index r with MODE_SPMM)
+    const int *perm;
+    const int64_t *rbeg;
+    const int64_t *rend;
 };
 
 // Per-chunk diagnostics.  PEAK_EXACT keeps, per lane slot, the running max of
@@ -258,14 +264,25 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
     for (int k = 0; k < (PEAK == PEAK_EXACT ? VPL : 1); ++k) pk[k] = 0ull;
     unsigned badmask = 0u;
 
-    auto row_of = [&](int64_t it) { return P.reverse ? (P.n_rows - 1 - it) : it; };
+    auto row_of = [&](int64_t it) -> int64_t {  // -1 for the idle tail groups of the last warp
+        if (it >= P.n_rows) return -1;
+        const int64_t i = P.reverse ? (P.n_rows - 1 - it) : it;
+        return P.perm ? (int64_t)__ldg(P.perm + i) : i;
+    };
+    auto extent = [&](int64_t r, int64_t &b, int64_t &e) {
+        if (P.rbeg) {
+            b = __ldg(P.rbeg + r);
+            e = __ldg(P.rend + r);
+        } else {
+            b = __ldg(P.rowptr + r);
+            e = __ldg(P.rowptr + r + 1);
+        }
+    };
     // current row's extent and first entry batch, loaded one row ahead
     int64_t it = warp * RPW + grp;
     int64_t beg = 0, end = 0;
     if (it < P.n_rows) {
-        const int64_t r = row_of(it);
-        beg = __ldg(P.rowptr + r);
-        end = __ldg(P.rowptr + r + 1);
+        extent(row_of(it), beg, end);
     }
     int myj = 0;
     T mya = (T)0;
@@ -293,9 +310,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
         const int64_t it2 = it + wstride;
         int64_t beg2 = 0, end2 = 0;
         if (it2 < P.n_rows) {
-            const int64_t r2 = row_of(it2);
-            beg2 = __ldg(P.rowptr + r2);
-            end2 = __ldg(P.rowptr + r2 + 1);
+            extent(row_of(it2), beg2, end2);
         }
         const int len = (int)(end - beg);
         const int nb_mine = (len + G - 1) / G;
@@ -453,6 +468,88 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
         __syncthreads();
         for (int c = threadIdx.x; c < nch; c += blockDim.x)
             if (s_peak[c]) atomicMax(&P.peaks[first_chunk + c], s_peak[c]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1c: heavy rows.  Rows longer than the split threshold are cut into fixed
+// chunks whose partial sums K1 computes in parallel (MODE_SPMM over the chunk
+// ranges, written to `partials`); this kernel adds a row's partials in chunk
+// order (deterministic, independent of the launch shape) and runs the same
+// fused epilogue as K1.  One warp per heavy row, lanes over the row's vectors.
+// ---------------------------------------------------------------------------
+struct HeavyParams {
+    const int *rows;        // heavy row ids
+    const int *chunk_off;   // chunks of heavy row h: [chunk_off[h], chunk_off[h+1])
+    const void *partials;   // n_chunks x ldv vectors
+    int n_heavy;
+};
+
+template <typename T, int MODE, int PEAK>
+__global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const HeavyParams H) {
+    typedef typename Vec<T>::type VT;
+    constexpr int W = Vec<T>::W;
+    constexpr int MS = 3;  // vectors per lane: a tile has at most 96 vectors
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const VT *part = (const VT *)H.partials + P.v0 + lane;
+    VT *yout = (VT *)P.yout;
+    VT *E = (VT *)P.E;
+    const T alpha = (T)P.alpha, beta = (T)P.beta, theta = (T)P.theta;
+    const bool has_prev = P.has_prev != 0;
+    const int first_chunk = (P.col0 + P.v0 * W) >> 5;
+    bool valid[MS];
+#pragma unroll
+    for (int k = 0; k < MS; ++k) valid[k] = (lane + 32 * k) < P.nvt;
+    unsigned long long pk[MS];
+#pragma unroll
+    for (int k = 0; k < MS; ++k) pk[k] = 0ull;
+    unsigned badmask = 0u;
+    for (int64_t h = warp; h < H.n_heavy; h += nwarps) {
+        const int64_t row = H.rows[h];
+        const int c0 = H.chunk_off[h], c1 = H.chunk_off[h + 1];
+        VT acc[MS];
+#pragma unroll
+        for (int k = 0; k < MS; ++k) acc[k] = vzero(VT());
+        for (int c = c0; c < c1; ++c) {
+#pragma unroll
+            for (int k = 0; k < MS; ++k)
+                if (valid[k]) acc[k] = vmadd(acc[k], (T)1, part[(int64_t)c * P.ldv + 32 * k]);
+        }
+        VT *yo = yout + row * (int64_t)P.ldv + P.v0 + lane;
+        if (MODE == MODE_SPMM) {
+#pragma unroll
+            for (int k = 0; k < MS; ++k)
+                if (valid[k]) yo[32 * k] = acc[k];
+            continue;
+        }
+        VT *er = E + row * (int64_t)P.ldv + P.v0 + lane;
+#pragma unroll
+        for (int k = 0; k < MS; ++k) {
+            if (!valid[k]) continue;
+            const VT p = has_prev ? ld_stream(yo + 32 * k) : vzero(VT());
+            const VT e = ld_stream(er + 32 * k);
+            const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
+            yo[32 * k] = q;
+            st_stream(er + 32 * k, vaccum(e, theta, q));
+            if (PEAK == PEAK_EXACT) {
+                const unsigned long long bq = vpeak(q);
+                pk[k] = bq > pk[k] ? bq : pk[k];
+            } else if (!vfinite(q)) {
+                badmask |= 1u << (((P.col0 + (P.v0 + lane + 32 * k) * W) >> 5) - first_chunk);
+            }
+        }
+    }
+    if (MODE == MODE_RECUR && P.peaks) {
+#pragma unroll
+        for (int k = 0; k < MS; ++k) {
+            if (PEAK == PEAK_EXACT && valid[k] && pk[k]) {
+                const int c = (P.col0 + (P.v0 + lane + 32 * k) * W) >> 5;
+                atomicMax(&P.peaks[c], pk[k]);
+            }
+        }
+        for (unsigned m = badmask; m; m &= m - 1) atomicMax(&P.peaks[first_chunk + __ffs(m) - 1], 0x7FF0000000000000ull);
     }
 }
 

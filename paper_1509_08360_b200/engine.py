@@ -191,6 +191,15 @@ class DeviceMatrix:
         """values *= factor in place (scale_values, sparse.py:295-301)."""
         _lib.check(self.lib.csemb_matrix_scale(self.handle, float(factor)), "csemb_matrix_scale")
 
+    def spectral_norm(self, iters: int, k: int, seed: int, safety: float = 1.01, v0=None) -> float:
+        """Device power iteration (estimate_spectral_norm, engine.py:165-192) on
+        this resident matrix; v0=None draws the start block with Philox."""
+        out = C.c_double(0.0)
+        v0 = None if v0 is None else np.ascontiguousarray(v0, dtype=np.float64)
+        _lib.check(self.lib.csemb_spectral_norm(self.handle, int(iters), int(k), _lib.ptr(v0), int(seed) & _M64,
+                                                float(safety), C.byref(out)), "csemb_spectral_norm")
+        return float(out.value)
+
     def download_values(self) -> np.ndarray:
         out = np.empty(self.nnz, dtype=np.float64)
         _lib.check(self.lib.csemb_matrix_download_values(self.handle, _lib.ptr(out)))
@@ -235,6 +244,16 @@ class Plan:
 
     def set_option(self, option: int, value: int) -> None:
         _lib.check(self.lib.csemb_plan_set_option(self.handle, int(option), int(value)), "csemb_plan_set_option")
+
+    def set_load_balance(self, split_threshold: int | None = None, row_order: int | None = None) -> None:
+        """Rows longer than split_threshold (default 4096; 0 = never) are split
+        into chunks summed in chunk order (no longer bit-identical to the
+        reference's sequential sum for those rows); row_order -1 auto /
+        0 natural / 1 bucketed by length.  Reordering never changes results."""
+        if split_threshold is not None:
+            self.set_option(_lib.OPT_SPLIT_THRESHOLD, int(split_threshold))
+        if row_order is not None:
+            self.set_option(_lib.OPT_ROW_ORDER, int(row_order))
 
     def set_exact_peaks(self, on: bool) -> None:
         """Record exact per-chunk max|Q(r)| (for the debug log) instead of flags."""
