@@ -145,6 +145,24 @@ int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int order, int n_
                           int64_t col0, int64_t d_global, int normalize_rows,
                           double *out_host, double *max_abs, int *first_bad_r, int *bad_stage);
 
+/* ---- row-partitioned runs (graphs larger than one GPU) ---------
+ * The plan's matrix holds rows [row0, row0 + n_rows) of an n_global x n_global
+ * operator (local CSR with GLOBAL column ids).  Each step gathers from the
+ * caller-owned full buffer full_dev (n_global x ld, plan dtype) holding Q(r-1)
+ * and writes the local Q(r) into q[r & 1] (q0_dev/q1_dev: caller-owned
+ * n_rows x ld buffers, or NULL for the plan's own).  Between steps the caller
+ * all-gathers the local Q(r) of every rank into full_dev (e.g. NCCL
+ * all_gather_into_tensor).  Stored-order accumulation per row is unchanged,
+ * so the assembled E is bit-identical to the single-GPU run.  */
+int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev, void *q0_dev,
+                         void *q1_dev);
+/* Stage init for the local rows (hash of the GLOBAL row index); for generated
+ * kinds also writes the full Q(0) into full_dev (no exchange before step 1). */
+int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, const double *block_dev,
+                     int omega_kind, uint64_t seed, int64_t col0, int64_t d_global);
+int csemb_plan_step(csemb_plan *p, int r); /* r = 1..order, asynchronous */
+int csemb_plan_end(csemb_plan *p, int normalize_rows);
+
 /* ---- projection block: sample_projection (engine.py:79-99) -----------------
  * Columns [col0, col0+w) of the n x d_global block, hashed with the global d.
  * kind CSEMB_OMEGA_SPLITMIX is bit-identical to the reference.  */

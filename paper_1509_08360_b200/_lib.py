@@ -66,6 +66,10 @@ SIGNATURES = {
     "csemb_plan_timing": (_int, [_p, _pf, _pf, _pi]),
     "csemb_apply_expansion": (
         _int, [_p, _p, _int, _int, _p, _int, _u64, _i64, _i64, _int, _p, _p, _pi, _pi]),
+    "csemb_plan_partition": (_int, [_p, _i64, _i64, _p, _p, _p]),
+    "csemb_plan_begin": (_int, [_p, _p, _int, _p, _int, _u64, _i64, _i64]),
+    "csemb_plan_step": (_int, [_p, _int]),
+    "csemb_plan_end": (_int, [_p, _int]),
     "csemb_sample_projection": (_int, [_p, _i64, _i64, _u64, _i64, _i64, _int, _p]),
     "csemb_rownorm": (_int, [_p, _p, _i64, _i64, _i64, _int]),
     "csemb_spectral_norm": (_int, [_p, _int, _i64, _p, _u64, _dbl, _pd]),

@@ -105,6 +105,15 @@ struct csemb_plan {
     int row_order = -1;              // -1 auto, 0 natural, 1 bucketed by batch count
     void *partials = nullptr;        // heavy-row chunk partial sums
     size_t partials_bytes = 0;
+    // row partition (csemb_plan_partition): this plan's matrix holds rows
+    // [row0, row0 + n_rows) of an n_global-row operator; steps gather from the
+    // caller-owned full Q(r-1) buffer and write the local Q(r) into q[r & 1]
+    bool partitioned = false;
+    int64_t row0 = 0, n_global = 0;
+    void *full = nullptr;
+    void *ext_q[2] = {nullptr, nullptr};
+    std::vector<double> coeffs;  // stage coefficients of the step-wise run
+    int64_t col0 = 0, d_global = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -649,7 +658,7 @@ static void plan_free(csemb_plan *p) {
 extern "C" int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out) {
     if (!m || !out) return fail(CSEMB_ERR_INVALID, "null argument");
     if (d < 1) return fail(CSEMB_ERR_INVALID, "d must be >= 1");
-    if (m->n_rows != m->n_cols) return fail(CSEMB_ERR_INVALID, "the recurrence needs a square (symmetric) matrix");
+    if (m->n_rows > m->n_cols) return fail(CSEMB_ERR_INVALID, "the recurrence needs a square (symmetric) matrix");
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     *out = nullptr;
     CK(cudaSetDevice(m->ctx->device));
@@ -800,6 +809,9 @@ static int plan_run_locked(csemb_plan *p, const double *coeffs, int order, int n
                            const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
                            int64_t d_global, int normalize_rows) {
     if (!coeffs) return fail(CSEMB_ERR_INVALID, "null coefficients");
+    if (p->m->n_rows != p->m->n_cols)
+        return fail(CSEMB_ERR_INVALID, "the recurrence needs a square (symmetric) matrix");
+    if (p->partitioned) return fail(CSEMB_ERR_INVALID, "a partitioned plan runs step-wise (csemb_plan_begin/step/end)");
     if (order < 0) return fail(CSEMB_ERR_INVALID, "order must be >= 0");
     if (n_stages < 1) return fail(CSEMB_ERR_INVALID, "n_stages must be >= 1");
     if (omega_kind < CSEMB_OMEGA_GIVEN || omega_kind > CSEMB_OMEGA_PHILOX)
@@ -988,6 +1000,158 @@ extern "C" int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int or
     rc = plan_download_locked(p, out_host, CSEMB_F64);
     if (rc) return rc;
     if (fr) return fail(CSEMB_ERR_DIVERGED, "iteration r=%d produced non-finite values (stage %d)", fr, fs);
+    return CSEMB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// row-partitioned, step-wise runs (multi-GPU graphs larger than one GPU)
+// ---------------------------------------------------------------------------
+extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev,
+                                    void *q0_dev, void *q1_dev) {
+    if (!p || !full_dev) return fail(CSEMB_ERR_INVALID, "null argument");
+    csemb_mat *m = p->m;
+    if (m->n_cols != n_global) return fail(CSEMB_ERR_INVALID, "local matrix must have n_global columns");
+    if (row0 < 0 || row0 + m->n_rows > n_global) return fail(CSEMB_ERR_INVALID, "row block outside [0, n_global)");
+    if ((q0_dev == nullptr) != (q1_dev == nullptr)) return fail(CSEMB_ERR_INVALID, "give both local buffers or neither");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    p->partitioned = true;
+    p->row0 = row0;
+    p->n_global = n_global;
+    p->full = full_dev;
+    p->ext_q[0] = q0_dev;
+    p->ext_q[1] = q1_dev;
+    return CSEMB_OK;
+}
+
+template <typename T>
+static int plan_begin_t(csemb_plan *p, const double *block_dev, int omega_kind, uint64_t seed) {
+    csemb_mat *m = p->m;
+    csemb_ctx *c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows;
+    const int d = (int)p->d, ld = (int)p->ld;
+    const int order = (int)p->coeffs.size() - 1;
+    const int64_t n_chunks = (p->d_global + 31) / 32;
+    const size_t need = (size_t)std::max(order, 0) * (size_t)n_chunks;
+    if (need > p->peaks_cap) {
+        cudaFree(p->peaks);
+        p->peaks = nullptr;
+        p->peaks_cap = 0;
+        CK(cudaMalloc(&p->peaks, sizeof(unsigned long long) * need));
+        p->peaks_cap = need;
+    }
+    if (need) CK(cudaMemsetAsync(p->peaks, 0, sizeof(unsigned long long) * need, s));
+    p->order = order;
+    p->n_stages = 1;
+    p->n_chunks = n_chunks;
+    p->step_launches = 0;
+    T *q0 = (T *)(p->ext_q[0] ? p->ext_q[0] : p->y[0]);
+    const double scale = 1.0 / std::sqrt((double)p->d_global);
+    CK(cudaEventRecord(p->ev[0], s));
+    if (n > 0)
+        k_stage_init<T><<<grid_for(n * (int64_t)ld, 256, c->sm_count, 16), 256, 0, s>>>(
+            block_dev, q0, (T *)p->E, n, d, ld, omega_kind, seed, p->col0, p->d_global, p->coeffs[0], scale, p->row0);
+    CK(cudaGetLastError());
+    if (omega_kind != OMEGA_GIVEN)  // every rank generates the whole Q(0): no exchange for step 1
+        k_omega_fill<T><<<grid_for(p->n_global * (int64_t)ld, 256, c->sm_count, 16), 256, 0, s>>>(
+            (T *)p->full, p->n_global, d, ld, omega_kind, seed, p->col0, p->d_global, scale);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(p->ev[1], s));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, const double *block_dev,
+                                int omega_kind, uint64_t seed, int64_t col0, int64_t d_global) {
+    if (!p || !coeffs) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (!p->partitioned) return fail(CSEMB_ERR_INVALID, "plan is not partitioned (csemb_plan_partition)");
+    if (order < 0) return fail(CSEMB_ERR_INVALID, "order must be >= 0");
+    if (omega_kind < CSEMB_OMEGA_GIVEN || omega_kind > CSEMB_OMEGA_PHILOX)
+        return fail(CSEMB_ERR_INVALID, "unknown omega kind %d", omega_kind);
+    if (omega_kind == CSEMB_OMEGA_GIVEN && !block_dev && p->m->n_rows > 0)
+        return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
+    if (d_global < p->d || col0 < 0 || col0 + p->d > d_global || col0 % vec_w(p->m->dtype) != 0)
+        return fail(CSEMB_ERR_INVALID, "bad column slice");
+    for (int r = 0; r <= order; ++r)
+        if (!std::isfinite(coeffs[r])) return fail(CSEMB_ERR_INVALID, "coefficients must be finite");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    p->coeffs.assign(coeffs, coeffs + order + 1);
+    p->col0 = col0;
+    p->d_global = d_global;
+    return p->m->dtype == CSEMB_F64 ? plan_begin_t<double>(p, block_dev, omega_kind, seed)
+                                    : plan_begin_t<float>(p, block_dev, omega_kind, seed);
+}
+
+template <typename T>
+static int plan_step_t(csemb_plan *p, int r) {
+    csemb_mat *m = p->m;
+    csemb_ctx *c = m->ctx;
+    const int64_t n = m->n_rows;
+    const int ldv = (int)(p->ld / Vec<T>::W);
+    if (n == 0) return CSEMB_OK;
+    Schedule *sc = nullptr;
+    int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold, p->row_order, &sc);
+    if (rc) return rc;
+    const size_t pbytes = (size_t)sc->n_chunks * (size_t)p->ld * sizeof(T);
+    if (pbytes > p->partials_bytes) {
+        cudaFree(p->partials);
+        p->partials = nullptr;
+        p->partials_bytes = 0;
+        CK(cudaMalloc(&p->partials, pbytes));
+        p->partials_bytes = pbytes;
+    }
+    StepParams P;
+    std::memset(&P, 0, sizeof P);
+    P.rowptr = m->rowptr;
+    P.cols = m->cols;
+    P.vals = m->vals;
+    P.ycur = p->full;  // full Q(r-1), refreshed by the caller's all-gather
+    P.yout = p->ext_q[r & 1] ? p->ext_q[r & 1] : p->y[r & 1];
+    P.E = p->E;
+    P.n_rows = n;
+    P.ldv = ldv;
+    P.nvt = ldv;
+    P.alpha = 2.0 - 1.0 / (double)r;
+    P.beta = 1.0 - 1.0 / (double)r;
+    P.theta = p->coeffs[r];
+    P.has_prev = r > 1;
+    P.reverse = 0;  // the gathered rows were written by every rank: no tail reuse
+    P.peaks = p->peaks + (size_t)(r - 1) * p->n_chunks;
+    P.col0 = (int)p->col0;
+    if (p->exact_peaks)
+        CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, sc, p->partials, c->stream, c->sm_count, &p->step_launches));
+    else
+        CK(launch_step<T, MODE_RECUR, PEAK_FLAG>(P, sc, p->partials, c->stream, c->sm_count, &p->step_launches));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_step(csemb_plan *p, int r) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (!p->partitioned || p->coeffs.empty()) return fail(CSEMB_ERR_INVALID, "call csemb_plan_begin first");
+    if (r < 1 || r >= (int)p->coeffs.size()) return fail(CSEMB_ERR_INVALID, "step %d outside [1, order]", r);
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    return p->m->dtype == CSEMB_F64 ? plan_step_t<double>(p, r) : plan_step_t<float>(p, r);
+}
+
+extern "C" int csemb_plan_end(csemb_plan *p, int normalize_rows) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (!p->partitioned || p->coeffs.empty()) return fail(CSEMB_ERR_INVALID, "call csemb_plan_begin first");
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    csemb_ctx *c = p->m->ctx;
+    CK(cudaSetDevice(c->device));
+    CK(cudaEventRecord(p->ev[2], c->stream));
+    const int64_t n = p->m->n_rows;
+    if (normalize_rows && n > 0) {
+        const int g = grid_for(n * 32, 256, c->sm_count, 8);
+        if (p->m->dtype == CSEMB_F64)
+            k_rownorm<double><<<g, 256, 0, c->stream>>>((double *)p->E, n, (int)p->d, (int)p->ld);
+        else
+            k_rownorm<float><<<g, 256, 0, c->stream>>>((float *)p->E, n, (int)p->d, (int)p->ld);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(p->ev[3], c->stream));
+    p->ran = true;
     return CSEMB_OK;
 }
 

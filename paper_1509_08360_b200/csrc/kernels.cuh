@@ -151,6 +151,9 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_DEPTH
 #define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
 #endif
+#ifndef K1_QSTORE_CS
+#define K1_QSTORE_CS 1  // store Q(r) evict-first (measured: <=1% faster than write-back)
+#endif
 #ifndef K1_EARLY_EPI
 #define K1_EARLY_EPI 0  // 1: issue the row set's Q(r-2)/E loads at the start of its last batch
 #endif
@@ -426,7 +429,11 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
 #if (K1_ABLATE & 4)
                         if (__double_as_longlong((double)vpeak(q)) == 12345) yo[k * G] = q;
 #else
+#if K1_QSTORE_CS
+                        st_stream(yo + k * G, q);
+#else
                         yo[k * G] = q;
+#endif
                         st_stream(er + k * G, vaccum(e, theta, q));
 #endif
                         if (PEAK == PEAK_EXACT) {
@@ -592,7 +599,7 @@ __device__ __forceinline__ bool omega_sign(int kind, uint64_t key, uint64_t seed
 template <typename T>
 __global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int64_t n, int d,
                              int ld, int kind, uint64_t seed, int64_t col0, int64_t d_global,
-                             double theta0, double scale) {
+                             double theta0, double scale, int64_t row0 = 0) {
     const uint64_t key = mix64(seed);
     const int64_t total = n * (int64_t)ld;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -606,7 +613,7 @@ __global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int6
             } else if (kind == OMEGA_GIVEN) {
                 v = (T)given[i * d + c];
             } else {
-                v = (T)(omega_sign(kind, key, seed, i, col0 + c, d_global) ? scale : -scale);
+                v = (T)(omega_sign(kind, key, seed, row0 + i, col0 + c, d_global) ? scale : -scale);
             }
             if (sizeof(T) == 8)
                 e = (T)__dmul_rn((double)theta0, (double)v);
@@ -615,6 +622,20 @@ __global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int6
         }
         y0[t] = v;
         E[t] = e;
+    }
+}
+
+// the full n x ld projection block (gather source of a row-partitioned run's first step)
+template <typename T>
+__global__ void k_omega_fill(T *F, int64_t n, int d, int ld, int kind, uint64_t seed, int64_t col0,
+                             int64_t d_global, double scale) {
+    const uint64_t key = mix64(seed);
+    const int64_t total = n * (int64_t)ld;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / ld;
+        const int c = (int)(t - i * ld);
+        F[t] = c < d ? (T)(omega_sign(kind, key, seed, i, col0 + c, d_global) ? scale : -scale) : (T)0;
     }
 }
 

@@ -103,9 +103,9 @@ def dilate(A: DeviceCSR) -> DeviceCSR:
 def from_host(S, device: int = 0) -> DeviceCSR:
     """Upload a host CSR into torch CUDA tensors."""
     d = torch.device(f"cuda:{device}")
-    return DeviceCSR(S.n_rows, S.n_cols, torch.as_tensor(S.row_offsets, device=d),
-                     torch.as_tensor(S.col_indices, device=d).to(torch.int32),
-                     torch.as_tensor(S.values, device=d))
+    return DeviceCSR(S.n_rows, S.n_cols, torch.tensor(S.row_offsets, device=d),
+                     torch.tensor(S.col_indices, device=d).to(torch.int32),
+                     torch.tensor(S.values, device=d))
 
 
 # -- seeded generators for configs 3 and 4 at full scale (SURVEY 8(d)) -----------

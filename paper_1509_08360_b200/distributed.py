@@ -103,3 +103,108 @@ def embed_column_sharded(S, coeffs, d: int, *, n_stages: int = 1, seed: int = 0,
         dm.ctx.sync()
     dm.close()
     return E, combine_peaks(peaks, group)
+
+
+# ---------------------------------------------------------------------------
+# Row partition (config 5: graphs larger than one GPU's HBM)
+# ---------------------------------------------------------------------------
+def row_blocks(n: int, world: int) -> tuple[int, list[tuple[int, int]]]:
+    """Contiguous row blocks of n_pad = ceil(n / world) rows (the last may be
+    shorter): the layout NCCL's equal-chunk all-gather needs."""
+    if n < 1 or world < 1:
+        raise ValueError("n and world must be positive")
+    n_pad = -(-n // world)
+    return n_pad, [(min(p * n_pad, n), min((p + 1) * n_pad, n)) for p in range(world)]
+
+
+def local_rows(S, lo: int, hi: int):
+    """Rows [lo, hi) of a CSR with their GLOBAL column ids (a rank's block)."""
+    from .sparse import SparseMatrix
+
+    S = SparseMatrix.of(S)
+    offs = S.row_offsets[lo:hi + 1]
+    return SparseMatrix(hi - lo, S.n_cols, offs - offs[0], S.col_indices[offs[0]:offs[-1]],
+                        S.values[offs[0]:offs[-1]], check=False)
+
+
+class DeviceRowEngine:
+    """One rank's share of a row-partitioned run on its GPU (C ABI step-wise
+    plan over caller-owned torch buffers)."""
+
+    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q):
+        from .engine import DeviceMatrix
+
+        self.dm = DeviceMatrix(S_local, "float64" if dtype == "f64" else "float32", device)
+        self.plan = self.dm.plan(d)
+        self.plan.partition(row0, n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        self.n_local, self.d = S_local.n_rows, d
+
+    def begin(self, coeffs, omega_kind, seed, col0, d_global):
+        self.plan.begin(coeffs, omega_kind=omega_kind, seed=seed, col0=col0, d_global=d_global)
+
+    def step(self, r):
+        self.plan.step(r)
+        self.dm.ctx.sync()  # the caller's all-gather reads the local Q(r) next
+
+    def end(self, normalize_rows):
+        import torch
+
+        self.plan.end(normalize_rows)
+        out = torch.empty((self.n_local, self.d), dtype=torch.float64 if self.dm.dtype == 0 else torch.float32,
+                          device=f"cuda:{self.dm.ctx.device}")
+        self.plan.copy_output_to(out.data_ptr(), self.d)
+        self.dm.ctx.sync()
+        peaks, _, _ = self.plan.diagnostics()
+        self.dm.close()
+        return out, peaks
+
+
+def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, seed: int = 0,
+                          omega_kind: str = "reference", dtype: str = "f64", normalize_rows: bool = False,
+                          group=None, device: int | None = None, engine_factory=None):
+    """E rows [row0, row0 + n_local) of f_L(S) Omega for a row-partitioned S.
+
+    Each rank holds its row block of S (global column ids); every step gathers
+    from a replicated full Q(r-1) that one all-gather of the ranks' local Q(r)
+    refreshes -- the one exchange per step.  The
+    projection is generated from the global row index on every rank, so no
+    exchange precedes step 1.  Per-row arithmetic is unchanged, so the
+    assembled E is bit-identical to the single-GPU result.  Returns the local
+    E rows (torch tensor) and the per-chunk diagnostics max-combined over ranks.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    n_pad, blocks = row_blocks(n_global, world)
+    if blocks[rank] != (row0, row0 + S_local.n_rows):
+        raise ValueError(f"rank {rank} must hold rows {blocks[rank]}, not [{row0}, {row0 + S_local.n_rows})")
+    if omega_kind not in ("reference", "philox"):
+        raise ValueError("the row-partitioned driver generates the projection (reference or philox)")
+    width = 2 if dtype == "f64" else 4
+    ld = -(-d // width) * width
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    on_gpu = engine_factory is None
+    dev = torch.device(f"cuda:{torch.cuda.current_device() if device is None else device}") if on_gpu \
+        else torch.device("cpu")
+    F = torch.zeros((world * n_pad, ld), dtype=tdt, device=dev)
+    q = [torch.zeros((n_pad, ld), dtype=tdt, device=dev) for _ in range(2)]
+    if on_gpu:
+        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F, q)
+    else:
+        eng = engine_factory(S_local, row0, n_global, d, dtype, F, q)
+    kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
+    eng.begin(coeffs, kind, seed, 0, d)
+    order = len(coeffs) - 1
+    parts = [F[p * n_pad:(p + 1) * n_pad] for p in range(world)]
+    for r in range(1, order + 1):
+        eng.step(r)
+        if r < order:  # refresh the replicated Q(r) for the next step
+            if dist.get_backend(group) == "nccl":
+                dist.all_gather_into_tensor(F, q[r & 1], group=group)
+            else:
+                dist.all_gather(parts, q[r & 1], group=group)
+    E, peaks = eng.end(normalize_rows)
+    return E, combine_peaks(peaks, group)

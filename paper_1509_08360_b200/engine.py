@@ -312,6 +312,29 @@ class Plan:
         _lib.check(self.lib.csemb_plan_output(self.handle, C.byref(p), C.byref(ld), C.byref(dt)))
         return int(p.value or 0), int(ld.value), int(dt.value)
 
+    # -- row-partitioned, step-wise runs (csemb_plan_partition/begin/step/end) --
+    def partition(self, row0: int, n_global: int, full_ptr: int, q0_ptr: int | None = None,
+                  q1_ptr: int | None = None) -> None:
+        _lib.check(self.lib.csemb_plan_partition(
+            self.handle, int(row0), int(n_global), C.c_void_p(full_ptr),
+            None if q0_ptr is None else C.c_void_p(q0_ptr), None if q1_ptr is None else C.c_void_p(q1_ptr)),
+            "csemb_plan_partition")
+
+    def begin(self, coeffs, *, block_dev: int | None = None, omega_kind: int = _lib.OMEGA_SPLITMIX, seed: int = 0,
+              col0: int = 0, d_global: int | None = None) -> None:
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        d_global = self.d if d_global is None else int(d_global)
+        _lib.check(self.lib.csemb_plan_begin(
+            self.handle, _lib.ptr(c), len(c) - 1, None if block_dev is None else C.c_void_p(block_dev),
+            int(omega_kind), int(seed) & _M64, int(col0), d_global), "csemb_plan_begin")
+        self.last = (len(c) - 1, 1, d_global, int(col0))
+
+    def step(self, r: int) -> None:
+        _lib.check(self.lib.csemb_plan_step(self.handle, int(r)), "csemb_plan_step")
+
+    def end(self, normalize_rows: bool = False) -> None:
+        _lib.check(self.lib.csemb_plan_end(self.handle, int(bool(normalize_rows))), "csemb_plan_end")
+
     def copy_output_to(self, dst_ptr: int, dst_ld: int) -> None:
         """Device-to-device copy of E into a caller buffer (e.g. a torch tensor)."""
         _lib.check(self.lib.csemb_plan_copy_output(self.handle, C.c_void_p(dst_ptr), int(dst_ld)),

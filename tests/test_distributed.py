@@ -104,3 +104,79 @@ def test_shard_boundaries():
     assert column_shards(80, 8, 2) == [(i * 10, i * 10 + 10) for i in range(8)]
     with pytest.raises(ValueError):
         column_shards(0, 2, 2)
+
+
+# ---------------------------------------------------------------------------
+# row partition (config 5 layout), oracle engine on CPU
+# ---------------------------------------------------------------------------
+class OracleRowEngine:
+    """CPU stand-in for DeviceRowEngine: same buffers, oracle arithmetic
+    (numpy restatement of one engine._run_stage step)."""
+
+    def __init__(self, S_local, row0, n_global, d, dtype, F, q):
+        self.S = O.CSR.of(S_local)
+        self.row0, self.n, self.N, self.d, self.F, self.q = row0, S_local.n_rows, n_global, d, F, q
+
+    def begin(self, coeffs, kind, seed, col0, d_global):
+        assert kind == 1  # reference hash
+        self.coeffs = coeffs
+        full = O.sample_projection(self.N, d_global, seed)
+        self.F[:self.N, :self.d] = torch.from_numpy(full)
+        q0 = full[self.row0:self.row0 + self.n]
+        self.q[0][:self.n, :self.d] = torch.from_numpy(q0)
+        self.E = coeffs[0] * q0
+        self.peaks = np.zeros((1, len(coeffs) - 1, (d_global + 31) // 32))
+
+    def step(self, r):
+        y = O.spmm(self.S, np.ascontiguousarray(self.F[:self.N, :self.d].numpy()))
+        alpha, beta = 2.0 - 1.0 / r, 1.0 - 1.0 / r
+        q = alpha * y
+        if r > 1:
+            q = q - beta * self.q[r & 1][:self.n, :self.d].numpy()
+        self.E = self.E + self.coeffs[r] * q
+        self.q[r & 1][:self.n, :self.d] = torch.from_numpy(q)
+
+    def end(self, normalize_rows):
+        return torch.from_numpy(self.E), self.peaks
+
+
+def _row_worker(rank, world, port, d, seed, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import embed_row_partitioned, local_rows, row_blocks
+
+        S, coeffs = _problem()
+        _, blocks = row_blocks(S.n_rows, world)
+        lo, hi = blocks[rank]
+        Sl = local_rows(_as_sparse(S), lo, hi)
+        E, _ = embed_row_partitioned(Sl, lo, S.n_rows, coeffs, d, seed=seed, engine_factory=OracleRowEngine)
+        np.save(result_path + f".{rank}.npy", E.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _as_sparse(S):
+    from paper_1509_08360_b200 import SparseMatrix
+
+    return SparseMatrix(S.n_rows, S.n_cols, S.row_offsets, S.col_indices, S.values)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_matches_single_process(tmp_path, world):
+    d, seed = 37, 5
+    out = str(tmp_path / "rows")
+    mp.start_processes(_row_worker, args=(world, _free_port(), d, seed, out), nprocs=world,
+                       start_method="spawn", join=True)
+    got = np.concatenate([np.load(out + f".{p}.npy") for p in range(world)])
+    S, coeffs = _problem()
+    ref, _, _ = O.run_stage(S, coeffs, O.sample_projection(S.n_rows, d, seed))
+    assert np.array_equal(got, ref)
+
+
+def test_row_blocks():
+    from paper_1509_08360_b200.distributed import row_blocks
+
+    assert row_blocks(10, 3) == (4, [(0, 4), (4, 8), (8, 10)])
+    assert row_blocks(2, 4) == (1, [(0, 1), (1, 2), (2, 2), (2, 2)])

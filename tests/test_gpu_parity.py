@@ -412,3 +412,68 @@ class TestDeviceBuild:
         rn = np.sqrt(np.bincount(np.repeat(np.arange(500), np.diff(H.row_offsets)), weights=H.values ** 2,
                                  minlength=500))
         assert np.allclose(rn[rn > 0], 1.0)
+
+
+# --------------------------------------------------------------------------
+# row partition (config 5 layout): emulated ranks on one GPU, NCCL driver at ws=1
+# --------------------------------------------------------------------------
+class TestRowPartition:
+    @pytest.mark.parametrize("dtype", ["float64", "float32"])
+    def test_emulated_ranks_bit_exact(self, dtype):
+        import torch
+
+        from paper_1509_08360_b200.distributed import local_rows, row_blocks
+
+        S = graphs.sbm(3001, 7, 10.0, 3.0, seed=4)
+        n, d, L = S.n_rows, 40, 12
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), L).coeffs
+        ref = pb.DeviceMatrix(S, dtype).plan(d).apply(th, 1, None, omega_kind=1, seed=3)
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        world = 3
+        n_pad, blocks = row_blocks(n, world)
+        F = torch.zeros((world * n_pad, d), dtype=tdt, device="cuda")
+        ranks = []
+        for lo, hi in blocks:
+            dm = pb.DeviceMatrix(local_rows(S, lo, hi), dtype)
+            plan = dm.plan(d)
+            q = [torch.zeros((n_pad, d), dtype=tdt, device="cuda") for _ in range(2)]
+            plan.partition(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+            plan.begin(th, omega_kind=1, seed=3)
+            ranks.append((lo, hi, dm, plan, q))
+        for r in range(1, L + 1):
+            for lo, hi, dm, plan, q in ranks:  # independent launches: no rank waits on another
+                plan.step(r)
+            for _, _, dm, _, _ in ranks:
+                dm.ctx.sync()
+            if r < L:
+                for lo, hi, dm, plan, q in ranks:  # the all-gather, emulated by copies
+                    F[lo:hi] = q[r & 1][:hi - lo]
+                torch.cuda.synchronize()
+        got = []
+        for lo, hi, dm, plan, q in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        assert np.array_equal(np.concatenate(got), ref)
+
+    def test_nccl_driver_world_one(self):
+        import socket
+
+        import torch
+        import torch.distributed as dist
+
+        from paper_1509_08360_b200.distributed import embed_row_partitioned
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        try:
+            S = graphs.sbm(2000, 4, 8.0, 2.0, seed=6)
+            th = pb.legendre_coefficients(pb.indicator_above(0.3), 9).coeffs
+            E, peaks = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0)
+            ref, _, _ = O.run_stage(O.CSR.of(S), th, O.sample_projection(S.n_rows, 24, 2))
+            assert np.array_equal(E.cpu().numpy(), ref)
+            assert np.all(np.isfinite(peaks)) and not np.any(peaks >= np.inf)
+        finally:
+            dist.destroy_process_group()
