@@ -71,6 +71,8 @@ struct Schedule {
     int64_t n_chunks = 0;
     int *hrows = nullptr, *hoff = nullptr;     // heavy rows and their chunk offsets
     int n_heavy = 0;
+    int *corder = nullptr;  // chunk execution order: by first column, so concurrently
+                            // running chunks gather neighbouring rows (L2 reuse)
 };
 
 struct csemb_mat {
@@ -124,6 +126,7 @@ static void sched_free(Schedule *sc) {
     cudaFree(sc->cend);
     cudaFree(sc->hrows);
     cudaFree(sc->hoff);
+    cudaFree(sc->corder);
     delete sc;
 }
 
@@ -237,7 +240,7 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
             StepParams C = P;
             C.rbeg = sc->cbeg;
             C.rend = sc->cend;
-            C.perm = nullptr;
+            C.perm = sc->corder;  // sweep position -> chunk id (partials are indexed by chunk id)
             C.n_rows = sc->n_chunks;
             C.yout = partials;
             C.E = nullptr;
@@ -340,6 +343,24 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
         if (e == cudaSuccess) e = cudaMemcpy(sc->cend, cend.data(), 8 * cend.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(sc->hrows, hrows.data(), 4 * hrows.size(), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(sc->hoff, hoff.data(), 4 * hoff.size(), cudaMemcpyHostToDevice);
+        // order the chunks by their first column (results do not depend on it)
+        int *first = nullptr;
+        std::vector<int> hfirst(cbeg.size());
+        if (e == cudaSuccess) e = cudaMalloc(&first, 4 * cbeg.size());
+        if (e == cudaSuccess) {
+            k_gather_cols<<<grid_for((int64_t)cbeg.size(), 256, m->ctx->sm_count), 256>>>(m->cols, sc->cbeg, first,
+                                                                                         (int64_t)cbeg.size());
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpy(hfirst.data(), first, 4 * cbeg.size(), cudaMemcpyDeviceToHost);
+        cudaFree(first);
+        if (e == cudaSuccess) {
+            std::vector<int> ord(cbeg.size());
+            for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hfirst[a] < hfirst[b]; });
+            e = cudaMalloc(&sc->corder, 4 * ord.size());
+            if (e == cudaSuccess) e = cudaMemcpy(sc->corder, ord.data(), 4 * ord.size(), cudaMemcpyHostToDevice);
+        }
     }
     if (e != cudaSuccess) {
         cudaGetLastError();

@@ -781,6 +781,12 @@ __global__ void k_unpack(const T *__restrict__ src, O *dst, int64_t n, int d, in
     }
 }
 
+// out[i] = cols[idx[i]] (first column of each heavy-row chunk, for scheduling)
+__global__ void k_gather_cols(const int *__restrict__ cols, const int64_t *__restrict__ idx, int *out, int64_t n) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = cols[idx[t]];
+}
+
 // CSR conversion: int64 -> int32 column indices (with range check), f64 -> T values
 __global__ void k_cols_to_i32(const int64_t *__restrict__ src, int *dst, int64_t cnt,
                               int64_t n_cols, int *bad) {
