@@ -151,6 +151,9 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_DEPTH
 #define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
 #endif
+#ifndef K1_BATCH
+#define K1_BATCH 0  // stored entries per warp-uniform batch (<= G; 0: B = G, measured best)
+#endif
 #ifndef K1_QSTORE_CS
 #define K1_QSTORE_CS 1  // store Q(r) evict-first (measured: <=1% faster than write-back)
 #endif
@@ -287,17 +290,20 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
     if (it < P.n_rows) {
         extent(row_of(it), beg, end);
     }
+    // stored entries advance in batches of B <= G (lanes gl < B hold the batch)
+    constexpr int B = (K1_BATCH > 0 && K1_BATCH < G) ? K1_BATCH : G;
+    static_assert(G % B == 0, "batch width must divide the group width");
     int myj = 0;
     T mya = (T)0;
-    if (beg + gl < end) {
+    if (gl < B && beg + gl < end) {
         myj = __ldcs(cols + beg + gl);
         mya = __ldcs(vals + beg + gl);
     }
 
     // gathers of the first D-1 entries of the current batch, carried across batches
     constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (sizeof(T) == 8 ? 4 : 2);
-    constexpr int D = (DEPTH < G) ? DEPTH : G;
-    static_assert(G % D == 0, "pipeline depth must divide the batch width");
+    constexpr int D = (DEPTH < B) ? DEPTH : B;
+    static_assert(B % D == 0, "pipeline depth must divide the batch width");
     VT buf[D][VPL];
 #pragma unroll
     for (int e = 0; e < D - 1; ++e) {
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
             extent(row_of(it2), beg2, end2);
         }
         const int len = (int)(end - beg);
-        const int nb_mine = (len + G - 1) / G;
+        const int nb_mine = (len + B - 1) / B;
         const int nb = __reduce_max_sync(0xFFFFFFFFu, (unsigned)nb_mine);
 
         VT acc[VPL];
@@ -345,28 +351,28 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
             T na = (T)0;
             int ncnt = 0;  // entries of that next batch for my row
             if (b + 1 < nb_mine) {
-                ncnt = len - (b + 1) * G;
-                if (beg + (b + 1) * G + gl < end) {
-                    nj = __ldcs(cols + beg + (b + 1) * G + gl);
-                    na = __ldcs(vals + beg + (b + 1) * G + gl);
+                ncnt = len - (b + 1) * B;
+                if (gl < B && beg + (b + 1) * B + gl < end) {
+                    nj = __ldcs(cols + beg + (b + 1) * B + gl);
+                    na = __ldcs(vals + beg + (b + 1) * B + gl);
                 }
             } else if (b + 1 >= nb) {
                 ncnt = (int)(end2 - beg2);
-                if (beg2 + gl < end2) {
+                if (gl < B && beg2 + gl < end2) {
                     nj = __ldcs(cols + beg2 + gl);
                     na = __ldcs(vals + beg2 + gl);
                 }
             }
-            const int cnt = len - b * G;  // entries of this batch for my row (may be <= 0)
+            const int cnt = len - b * B;  // entries of this batch for my row (may be <= 0)
             // branch-free pipeline, D entries deep: step t issues the gathers of entry
             // t+D-1 (spilling into the NEXT batch's first entries near the end, so no
             // batch or row-set epilogue starts with an empty pipeline) and consumes t
 #pragma unroll
-            for (int t = 0; t < G; ++t) {
+            for (int t = 0; t < B; ++t) {
                 const int e = t + D - 1;
-                const int j = (e < G) ? __shfl_sync(0xFFFFFFFFu, myj, e % G, G)
-                                      : __shfl_sync(0xFFFFFFFFu, nj, e % G, G);
-                const bool more = (e < G) ? (e < cnt) : (e - G < ncnt);
+                const int j = (e < B) ? __shfl_sync(0xFFFFFFFFu, myj, e % B, G)
+                                      : __shfl_sync(0xFFFFFFFFu, nj, e % B, G);
+                const bool more = (e < B) ? (e < cnt) : (e - B < ncnt);
 #if (K1_ABLATE & 2)
                 const VT *x = ycur + row * (int64_t)P.ldv;
 #else
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
         if (nb == 0) {  // every row of the warp is empty: move to the next rows' first batch
             myj = 0;
             mya = (T)0;
-            if (beg2 + gl < end2) {
+            if (gl < B && beg2 + gl < end2) {
                 myj = __ldcs(cols + beg2 + gl);
                 mya = __ldcs(vals + beg2 + gl);
             }
