@@ -302,6 +302,61 @@ def gen_builders():
     _save("builders", meta, **arrays)
 
 
+def gen_cli():
+    """The reference CLI (cli.py main) on three small inputs: an edge list
+    (normalized adjacency, cascade b=2), a raw symmetric Matrix Market matrix
+    (norm-estimate rescaling) and a rectangular one (dilation)."""
+    import tempfile
+
+    import scipy.io
+    import scipy.sparse as sp
+    from csemb import io as cio
+    from csemb.cli import main
+
+    arrays, meta = {}, {}
+    edges, _ = sbm(120, 4, 0.3, 0.02, np.random.default_rng(88))
+    rng = np.random.default_rng(9)
+    raw = random_symmetric(60, rng, density=0.15, spectral_norm=None) * 3.0
+    rect = rng.random((40, 25)) * (rng.random((40, 25)) < 0.3)
+    arrays["edges"] = edges.astype(np.int64)
+    arrays["raw"] = raw
+    arrays["rect"] = rect
+    drop = ("wall_time_s", "input", "output")
+    with tempfile.TemporaryDirectory() as tmp:
+        g = os.path.join(tmp, "g.txt")
+        with open(g, "w") as fh:
+            fh.write("\n".join(f"{u} {v}" for u, v in edges) + "\n")
+        scipy.io.mmwrite(os.path.join(tmp, "raw.mtx"), sp.coo_array(raw))
+        scipy.io.mmwrite(os.path.join(tmp, "rect.mtx"), sp.coo_array(rect))
+        runs = {
+            "edgelist": ["embed", "--input", g, "--format", "edgelist", "--matrix", "normalized-adjacency",
+                         "--function", "indicator:0.3", "--L", "48", "--b", "2", "--d", "40", "--seed", "123"],
+            "raw": ["embed", "--input", os.path.join(tmp, "raw.mtx"), "--format", "matrix-market",
+                    "--matrix", "raw", "--function", "indicator:0.2", "--L", "20", "--d", "16", "--seed", "5"],
+            "dilation": ["embed", "--input", os.path.join(tmp, "rect.mtx"), "--format", "matrix-market",
+                         "--matrix", "dilation", "--function", "indicator:0.3", "--L", "30", "--d", "12",
+                         "--seed", "6"],
+        }
+        for name, argv in runs.items():
+            out = os.path.join(tmp, name + ".bin")
+            cols = os.path.join(tmp, name + ".cols.bin")
+            extra = ["--output-cols", cols] if name == "dilation" else []
+            assert main(argv + ["--output", out] + extra) == 0
+            with open(out, "rb") as fh:
+                blob = fh.read()
+            arrays[f"{name}_E"] = cio.read_embedding(out)
+            if extra:
+                arrays[f"{name}_cols"] = cio.read_embedding(cols)
+            md = json.load(open(out + ".meta.json"))
+            meta[name] = {"argv": argv, "sha256": hashlib.sha256(blob).hexdigest(),
+                          "metadata": {k: v for k, v in md.items() if k not in drop}}
+        ns = os.path.join(tmp, "norm.json")
+        assert main(["norm", "--input", os.path.join(tmp, "raw.mtx"), "--format", "matrix-market", "--matrix", "raw",
+                     "--seed", "3", "--output", ns]) == 0
+        meta["norm"] = json.load(open(ns))
+    _save("cli", meta, **arrays)
+
+
 if __name__ == "__main__":
     gen_omega()
     gen_config1()
@@ -309,3 +364,4 @@ if __name__ == "__main__":
     gen_coefficients()
     gen_norm()
     gen_builders()
+    gen_cli()

@@ -7,7 +7,9 @@ Frobenius error <= 1e-4 vs the fp64 reference and pairwise cosine error
 """
 
 import hashlib
+import json
 import logging
+import os
 
 import numpy as np
 import pytest
@@ -477,3 +479,64 @@ class TestRowPartition:
             assert np.all(np.isfinite(peaks)) and not np.any(peaks >= np.inf)
         finally:
             dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------
+# CLI drop-in: the reference's own command lines, outputs compared
+# --------------------------------------------------------------------------
+class TestCLI:
+    def _inputs(self, tmp_path):
+        import scipy.io
+        import scipy.sparse as sp
+
+        z, meta = load_golden("cli")
+        g = tmp_path / "g.txt"
+        g.write_text("\n".join(f"{u} {v}" for u, v in z["edges"]) + "\n")
+        scipy.io.mmwrite(str(tmp_path / "raw.mtx"), sp.coo_array(z["raw"]))
+        scipy.io.mmwrite(str(tmp_path / "rect.mtx"), sp.coo_array(z["rect"]))
+        return z, meta
+
+    def _argv(self, meta, name, tmp_path):
+        argv = list(meta[name]["argv"])
+        i = argv.index("--input")
+        argv[i + 1] = str(tmp_path / os.path.basename(argv[i + 1]))
+        return argv
+
+    def test_edgelist_byte_identical(self, tmp_path):
+        from paper_1509_08360_b200.cli import main
+
+        z, meta = self._inputs(tmp_path)
+        out = str(tmp_path / "e.bin")
+        assert main(self._argv(meta, "edgelist", tmp_path) + ["--output", out]) == 0
+        assert hashlib.sha256(open(out, "rb").read()).hexdigest() == meta["edgelist"]["sha256"]
+        md = json.load(open(out + ".meta.json"))
+        for k, v in meta["edgelist"]["metadata"].items():
+            assert md[k] == v, k
+
+    def test_raw_and_dilation(self, tmp_path):
+        from paper_1509_08360_b200 import io as bio
+        from paper_1509_08360_b200.cli import main
+
+        z, meta = self._inputs(tmp_path)
+        out = str(tmp_path / "r.bin")
+        assert main(self._argv(meta, "raw", tmp_path) + ["--output", out]) == 0
+        assert rel(bio.read_embedding(out), z["raw_E"]) <= 1e-12
+        md = json.load(open(out + ".meta.json"))
+        assert md["norm_estimate"] == pytest.approx(meta["raw"]["metadata"]["norm_estimate"], rel=1e-12)
+        assert md["spmv_products"] == meta["raw"]["metadata"]["spmv_products"]
+        out = str(tmp_path / "d.bin")
+        cols = str(tmp_path / "d.cols.bin")
+        assert main(self._argv(meta, "dilation", tmp_path) + ["--output", out, "--output-cols", cols]) == 0
+        assert rel(bio.read_embedding(out), z["dilation_E"]) <= 1e-12
+        assert rel(bio.read_embedding(cols), z["dilation_cols"]) <= 1e-12
+        md = json.load(open(out + ".meta.json"))
+        assert md["coeffs_sha256"] == meta["dilation"]["metadata"]["coeffs_sha256"]
+
+    def test_norm_command(self, tmp_path, capsys):
+        from paper_1509_08360_b200.cli import main
+
+        z, meta = self._inputs(tmp_path)
+        assert main(["norm", "--input", str(tmp_path / "raw.mtx"), "--format", "matrix-market", "--matrix", "raw",
+                     "--seed", "3"]) == 0
+        got = json.loads(capsys.readouterr().out)
+        assert got["norm_estimate"] == pytest.approx(meta["norm"]["norm_estimate"], rel=1e-12)

@@ -204,3 +204,51 @@ def test_product_never_imports_oracle():
     for p in pkg.rglob("*.py"):
         src = p.read_text()
         assert "import oracle" not in src and "from oracle" not in src, p
+
+
+class TestIOAndCLI:
+    def test_embedding_round_trip(self, tmp_path):
+        from paper_1509_08360_b200 import io as bio
+
+        v = np.random.default_rng(0).standard_normal((7, 3))
+        p = str(tmp_path / "e.bin")
+        bio.write_embedding(p, v)
+        raw = open(p, "rb").read()
+        assert raw[:8] == b"CSEMB001" and len(raw) == 8 + 16 + 8 * 21
+        assert np.array_equal(bio.read_embedding(p), v)
+        open(p, "wb").write(b"XXXX")
+        with pytest.raises(pb.InputFormatError):
+            bio.read_embedding(p)
+
+    def test_edgelist_reader(self, tmp_path):
+        from paper_1509_08360_b200 import io as bio
+
+        p = tmp_path / "g.txt"
+        p.write_text("# comment\n0 1\n1 2\n")
+        e, n = bio.read_edgelist(str(p))
+        assert n == 3 and e.shape == (2, 2)
+        p.write_text("0 -1\n")
+        with pytest.raises(pb.InputFormatError):
+            bio.read_edgelist(str(p))
+
+    def test_usage_errors_exit_2(self, tmp_path):
+        from paper_1509_08360_b200.cli import main
+
+        g = tmp_path / "g.txt"
+        g.write_text("0 1\n")
+        with pytest.raises(SystemExit) as ex:
+            main(["embed", "--input", str(g), "--format", "edgelist", "--matrix", "raw", "--function",
+                  "indicator:0.5", "--L", "4", "--output", str(tmp_path / "o.bin")])
+        assert ex.value.code == 2
+        with pytest.raises(SystemExit) as ex:
+            main(["embed", "--input", str(g), "--format", "edgelist", "--function", "bogus", "--L", "4",
+                  "--output", str(tmp_path / "o.bin")])
+        assert ex.value.code == 2
+
+    def test_parse_error_exit_3(self, tmp_path):
+        from paper_1509_08360_b200.cli import main
+
+        g = tmp_path / "g.txt"
+        g.write_text("zero one\n")
+        assert main(["embed", "--input", str(g), "--format", "edgelist", "--function", "indicator:0.5", "--L", "4",
+                     "--output", str(tmp_path / "o.bin")]) == 3
