@@ -109,6 +109,9 @@ int csemb_plan_destroy(csemb_plan *p);
                                        0 = never split (bit-exact for every input) */
 #define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default), 0 natural, 1 bucketed by
                                        batch count (skewed row lengths) */
+#define CSEMB_OPT_E_FOLD 5           /* 1..3 (default 3): E is read and written every
+                                       e_fold steps; a flush adds the pending terms in
+                                       the reference's order, so results are unchanged */
 int csemb_plan_set_option(csemb_plan *p, int option, int64_t value);
 
 /* Device-resident run: _apply_expansion (engine.py:231-258) chained over

@@ -104,6 +104,7 @@ struct csemb_plan {
     int exact_peaks = 0;
     int reverse_sweep = 1;
     int64_t split_threshold = 4096;  // 0: never split rows (bit-exact for every input)
+    int e_fold = 3;                  // E read/written every e_fold steps (1..3), same roundings
     int row_order = -1;              // -1 auto, 0 natural, 1 bucketed by batch count
     void *partials = nullptr;        // heavy-row chunk partial sums
     size_t partials_bytes = 0;
@@ -275,6 +276,18 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
     }
     if (launches) *launches += nl;
     return cudaSuccess;
+}
+
+// E-update folding for step r of an order-L stage: flush every K steps and at
+// the last step, adding the pending terms r-2 / r-1 / r in order (bits 4/2/1).
+static int efold_bits(int r, int L, int K) {
+    if (K <= 1) return 1;
+    if (r % K != 0 && r != L) return 0;
+    const int first = ((r - 1) / K) * K + 1;  // first step not yet added to E
+    int bits = 1;
+    if (first <= r - 1) bits |= 2;
+    if (first <= r - 2) bits |= 4;
+    return bits;
 }
 
 static const int64_t HEAVY_CHUNK = 1024;  // entries per chunk of a split heavy row
@@ -717,6 +730,10 @@ extern "C" int csemb_plan_set_option(csemb_plan *p, int option, int64_t value) {
             if (value < 0) return fail(CSEMB_ERR_INVALID, "split threshold must be >= 0");
             p->split_threshold = value;
             return CSEMB_OK;
+        case CSEMB_OPT_E_FOLD:
+            if (value < 1 || value > 3) return fail(CSEMB_ERR_INVALID, "E fold must be 1, 2 or 3");
+            p->e_fold = (int)value;
+            return CSEMB_OK;
         case CSEMB_OPT_ROW_ORDER:
             if (value < -1 || value > 1) return fail(CSEMB_ERR_INVALID, "row order must be -1, 0 or 1");
             p->row_order = (int)value;
@@ -803,6 +820,9 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
             P.alpha = 2.0 - 1.0 / (double)r;  // engine.py:214, same IEEE expression
             P.beta = 1.0 - 1.0 / (double)r;   // engine.py:216
             P.theta = coeffs[r];
+            P.efold = efold_bits(r, order, p->e_fold);
+            P.theta1 = r >= 2 ? coeffs[r - 1] : 0.0;
+            P.theta2 = r >= 3 ? coeffs[r - 2] : 0.0;
             P.has_prev = r > 1;
             P.reverse = p->reverse_sweep && (r & 1) == 0;
             P.peaks = p->peaks + ((size_t)st * order + (r - 1)) * n_chunks;
@@ -1135,6 +1155,11 @@ static int plan_step_t(csemb_plan *p, int r) {
     P.alpha = 2.0 - 1.0 / (double)r;
     P.beta = 1.0 - 1.0 / (double)r;
     P.theta = p->coeffs[r];
+    const int L = (int)p->coeffs.size() - 1;
+    P.efold = efold_bits(r, L, p->e_fold);
+    P.theta1 = r >= 2 ? p->coeffs[r - 1] : 0.0;
+    P.theta2 = r >= 3 ? p->coeffs[r - 2] : 0.0;
+    P.row_base = p->row0;  // the gather source holds global rows
     P.has_prev = r > 1;
     P.reverse = 0;  // the gathered rows were written by every rank: no tail reuse
     P.peaks = p->peaks + (size_t)(r - 1) * p->n_chunks;

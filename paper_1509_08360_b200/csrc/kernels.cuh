@@ -117,6 +117,13 @@ struct StepParams {
     int v0;            // first vector of this column tile
     int nvt;           // vectors in this column tile
     double alpha, beta, theta;
+    // E update folding: E is read/written only on flush steps, which add the
+    // pending terms in the reference's order, ((E + th2*Q(r-2)) + th1*Q(r-1)) + th*Q(r):
+    // efold bit 1 = flush (add th*Q(r)), bit 2 = add th1*Q(r-1) (the row's own
+    // row of the gather source), bit 4 = add th2*Q(r-2) (the loaded old value)
+    int efold;
+    double theta1, theta2;
+    int64_t row_base;  // global index of local row 0 in the gather source (row partition)
     int has_prev;
     int reverse;       // sweep rows in descending order (L2 reuse of the tail)
     unsigned long long *peaks;  // this step's per-chunk max|Q| keys (MODE_RECUR), or null
@@ -146,7 +153,7 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 }
 
 #ifndef K1_MIN_BLOCKS
-#define K1_MIN_BLOCKS 0  // 0: 2 CTAs/SM for fp64 (128 registers), 3 for fp32 (80 registers)
+#define K1_MIN_BLOCKS 0  // 0: 2 CTAs/SM (128 registers) for both dtypes (measured best)
 #endif
 #ifndef K1_DEPTH
 #define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
@@ -156,9 +163,6 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #endif
 #ifndef K1_QSTORE_CS
 #define K1_QSTORE_CS 1  // store Q(r) evict-first (measured: <=1% faster than write-back)
-#endif
-#ifndef K1_EARLY_EPI
-#define K1_EARLY_EPI 0  // 1: issue the row set's Q(r-2)/E loads at the start of its last batch
 #endif
 #ifndef K1_ABLATE
 #define K1_ABLATE 0  // timing experiments only (results are wrong when nonzero)
@@ -243,7 +247,7 @@ __device__ __forceinline__ float4 vsel(bool c, float4 a, float4 b) {
 // gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
 // evict-first so L2 keeps the gathered rows of Q(r-1).
 template <typename T, int G, int VPL, int MODE, int PEAK>
-__global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(T) == 8 ? 2 : 3))) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_step(const StepParams P) {
     typedef typename Vec<T>::type VT;
     constexpr int W = Vec<T>::W;
     constexpr int RPW = 32 / G;  // rows per warp
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
     VT *yout = (VT *)P.yout;
     VT *E = (VT *)P.E;
     const T alpha = (T)P.alpha, beta = (T)P.beta, theta = (T)P.theta;
+    const T theta1 = (T)P.theta1, theta2 = (T)P.theta2;
     const bool has_prev = P.has_prev != 0;
     const int first_chunk = (P.col0 + P.v0 * W) >> 5;
 
@@ -329,23 +334,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
 #pragma unroll
         for (int k = 0; k < VPL; ++k) acc[k] = vzero(VT());
 
-        VT *const yo_row = yout + row * (int64_t)P.ldv + P.v0 + gl;
-        VT *const er_row = E + row * (int64_t)P.ldv + P.v0 + gl;
-        VT pv[VPL], ev[VPL];  // this row set's streamed epilogue operands
-#if K1_EARLY_EPI
-        const bool early = MODE == MODE_RECUR;
-#else
-        const bool early = false;
-#endif
         for (int b = 0; b < nb; ++b) {
-            if (early && b == nb - 1) {  // warp-uniform: overlap them with the last batch's gathers
-#pragma unroll
-                for (int k = 0; k < VPL; ++k) {
-                    const bool ok = active && valid[k];
-                    pv[k] = (ok && has_prev) ? ld_stream(yo_row + k * G) : vzero(VT());
-                    ev[k] = ok ? ld_stream(er_row + k * G) : vzero(VT());
-                }
-            }
             // prefetch the next batch of this row, else the next row's first batch
             int nj = 0;
             T na = (T)0;
@@ -421,17 +410,24 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
                     if (valid[k]) yo[k * G] = acc[k];
             } else {
                 VT *er = E + row * (int64_t)P.ldv + P.v0 + gl;
+                const VT *own = ycur + (P.row_base + row) * (int64_t)P.ldv;  // this row of Q(r-1)
+                // issue every streamed load of the epilogue before any arithmetic
+                VT pv[VPL], ev[VPL], ov[VPL];
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    pv[k] = ev[k] = ov[k] = vzero(VT());
+                    if (valid[k]) {
+#if !(K1_ABLATE & 1)
+                        if (has_prev) pv[k] = ld_stream(yo + k * G);
+                        if (P.efold) ev[k] = ld_stream(er + k * G);
+                        if (P.efold & 2) ov[k] = ld_gather(own + k * G);
+#endif
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < VPL; ++k) {
                     if (valid[k]) {
-#if (K1_ABLATE & 1)
-                        const VT p = vzero(VT()), e = vzero(VT());
-#else
-                        const bool had = early && nb > 0;
-                        const VT p = had ? pv[k] : (has_prev ? ld_stream(yo + k * G) : vzero(VT()));
-                        const VT e = had ? ev[k] : ld_stream(er + k * G);
-#endif
-                        const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
+                        const VT q = vrecur(acc[k], alpha, beta, pv[k], has_prev);
 #if (K1_ABLATE & 4)
                         if (__double_as_longlong((double)vpeak(q)) == 12345) yo[k * G] = q;
 #else
@@ -440,7 +436,12 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : (sizeof(
 #else
                         yo[k * G] = q;
 #endif
-                        st_stream(er + k * G, vaccum(e, theta, q));
+                        if (P.efold) {  // ((E + th2*Q(r-2)) + th1*Q(r-1)) + th*Q(r), the reference's order
+                            VT e = ev[k];
+                            if (P.efold & 4) e = vaccum(e, theta2, pv[k]);
+                            if (P.efold & 2) e = vaccum(e, theta1, ov[k]);
+                            st_stream(er + k * G, vaccum(e, theta, q));
+                        }
 #endif
                         if (PEAK == PEAK_EXACT) {
                             const unsigned long long bq = vpeak(q);
@@ -538,14 +539,19 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
             continue;
         }
         VT *er = E + row * (int64_t)P.ldv + P.v0 + lane;
+        const VT *own = (const VT *)P.ycur + (P.row_base + row) * (int64_t)P.ldv + P.v0 + lane;
 #pragma unroll
         for (int k = 0; k < MS; ++k) {
             if (!valid[k]) continue;
             const VT p = has_prev ? ld_stream(yo + 32 * k) : vzero(VT());
-            const VT e = ld_stream(er + 32 * k);
             const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
             yo[32 * k] = q;
-            st_stream(er + 32 * k, vaccum(e, theta, q));
+            if (P.efold) {
+                VT e = ld_stream(er + 32 * k);
+                if (P.efold & 4) e = vaccum(e, (T)P.theta2, p);
+                if (P.efold & 2) e = vaccum(e, (T)P.theta1, ld_gather(own + 32 * k));
+                st_stream(er + 32 * k, vaccum(e, theta, q));
+            }
             if (PEAK == PEAK_EXACT) {
                 const unsigned long long bq = vpeak(q);
                 pk[k] = bq > pk[k] ? bq : pk[k];

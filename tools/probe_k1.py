@@ -25,6 +25,7 @@ ap.add_argument("--L", type=int, default=6)
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--graphs", default="band,sbm,random")
 ap.add_argument("--widths", default="80")
+ap.add_argument("--efold", type=int, default=None)
 args = ap.parse_args()
 n = args.n
 
@@ -45,6 +46,8 @@ for name in args.graphs.split(","):
     for dt, w in [(dt, int(w)) for dt in args.dtype.split(",") for w in args.widths.split(",")]:
         dm = pb.DeviceMatrix(S, "float64" if dt == "f64" else "float32")
         plan = dm.plan(w)
+        if args.efold:
+            plan.set_option(_lib.OPT_E_FOLD, args.efold)
         best = 1e9
         for _ in range(3):
             plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
