@@ -540,3 +540,28 @@ class TestCLI:
                      "--seed", "3"]) == 0
         got = json.loads(capsys.readouterr().out)
         assert got["norm_estimate"] == pytest.approx(meta["norm"]["norm_estimate"], rel=1e-12)
+
+
+class TestEFold:
+    """E is read/written every 3 steps with the pending terms added in the
+    reference's order: every L (all flush patterns) stays bit-exact."""
+
+    @pytest.mark.parametrize("L", list(range(0, 9)))
+    def test_orders_bit_exact(self, L):
+        S = graphs.sbm(1500, 5, 8.0, 2.0, seed=L)
+        om = O.sample_projection(1500, 24, L)
+        th = np.random.default_rng(L).standard_normal(L + 1) * 0.4
+        ref = _oracle_embed(S, th, om)
+        for fold in (1, 2, 3):
+            plan = pb.device_matrix(S).plan(24)
+            plan.set_option(pb._lib.OPT_E_FOLD, fold)
+            assert np.array_equal(plan.apply(th, 1, om), ref), (L, fold)
+            plan.set_option(pb._lib.OPT_E_FOLD, 3)
+
+    def test_cascade_stages(self):
+        S = graphs.sbm(1200, 4, 8.0, 2.0, seed=9)
+        om = O.sample_projection(1200, 16, 9)
+        th = np.random.default_rng(9).standard_normal(8) * 0.4
+        ref, _, _ = O.apply_expansion(O.CSR.of(S), th, om, n_stages=3)
+        got = pb.device_matrix(S).plan(16).apply(th, 3, om)
+        assert np.array_equal(got, ref)
