@@ -148,28 +148,59 @@ static int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 
 static std::mutex g_occ_mu;
 static std::unordered_map<const void *, int> g_occ;
 
-template <typename T, int G, int VPL, int MODE, int PEAK>
-static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
-    const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK>;
+// Staged (TMA bulk-copy) K1 variant for groups of >= 8 lanes; CSEMB_K1_TMA=0/1
+// overrides the default.
+static int use_tma() {
+    static int on = [] {
+        const char *e = getenv("CSEMB_K1_TMA");
+        return e ? atoi(e) : 0;
+    }();
+    return on;
+}
+
+template <typename T, int G, int VPL, int MODE, int PEAK, bool STAGED>
+static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count) {
+    const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK, STAGED>;
     const int threads = 256;
     const int W = Vec<T>::W;
-    const int nch = ((P.col0 + (P.v0 + P.nvt) * W - 1) >> 5) - ((P.col0 + P.v0 * W) >> 5) + 1;
-    const size_t smem = MODE == MODE_RECUR ? (size_t)(nch + 1) * 8 : 0;
+    const int nch = ((P0.col0 + (P0.v0 + P0.nvt) * W - 1) >> 5) - ((P0.col0 + P0.v0 * W) >> 5) + 1;
+    StepParams P = P0;
+    size_t smem = MODE == MODE_RECUR ? (size_t)(nch + 1) * 8 : 0;
+    size_t max_smem = 1024;
+    if (STAGED) {
+        constexpr int RPW = 32 / G;
+        constexpr int S = K1T_STAGES < G ? K1T_STAGES : G;
+        P.smem_base = (int)((smem + 127) / 128 * 128);
+        smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
+        max_smem = smem;
+    }
     int per_sm;
     {
         std::lock_guard<std::mutex> lk(g_occ_mu);
-        auto it = g_occ.find(fn);
+        const void *key = STAGED ? (const void *)((const char *)fn + P.nvt) : fn;  // staged: per tile width
+        auto it = g_occ.find(key);
         if (it == g_occ.end()) {
-            int nb = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, 1024);
+            cudaError_t e = cudaSuccess;
+            if (STAGED) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
             if (e != cudaSuccess) return e;
-            it = g_occ.emplace(fn, std::max(1, nb)).first;
+            int nb = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, max_smem);
+            if (e != cudaSuccess) return e;
+            it = g_occ.emplace(key, std::max(1, nb)).first;
         }
         per_sm = it->second;
     }
     const int grid = grid_for(P.n_rows * G, threads, sm_count, per_sm);
-    k_step<T, G, VPL, MODE, PEAK><<<grid, threads, smem, s>>>(P);
+    k_step<T, G, VPL, MODE, PEAK, STAGED><<<grid, threads, smem, s>>>(P);
     return cudaGetLastError();
+}
+
+template <typename T, int G, int VPL, int MODE, int PEAK>
+static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
+    if constexpr (G >= 8) {
+        if (use_tma()) return run_step_t<T, G, VPL, MODE, PEAK, true>(P, s, sm_count);
+    }
+    return run_step_t<T, G, VPL, MODE, PEAK, false>(P, s, sm_count);
 }
 
 // VPL instantiations: 1..3 for G == 1, 2..3 for wider groups (more vectors per

@@ -124,6 +124,7 @@ struct StepParams {
     int efold;
     double theta1, theta2;
     int64_t row_base;  // global index of local row 0 in the gather source (row partition)
+    int smem_base;     // staged variant: byte offset of the per-warp rings (after the peak slots)
     int has_prev;
     int reverse;       // sweep rows in descending order (L2 reuse of the tail)
     unsigned long long *peaks;  // this step's per-chunk max|Q| keys (MODE_RECUR), or null
@@ -235,6 +236,32 @@ __device__ __forceinline__ float4 vsel(bool c, float4 a, float4 b) {
     return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
 }
 
+// ---- TMA bulk copies + mbarriers (staged K1) ----------------------------------
+#ifndef K1T_STAGES
+#define K1T_STAGES 8  // neighbour rows in flight per group in the staged variant
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
+// one neighbour-row tile (global -> shared), completion counted on `bar`
+__device__ __forceinline__ void tma_row(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // K1: one recurrence step (MODE_RECUR) or a plain multi-vector SpMM (MODE_SPMM).
 // A group of G lanes owns a row; lane gl holds the 16-byte vectors gl + k*G
 // (k < VPL) of the row's column tile.  The warp's 32/G rows advance together
@@ -246,8 +273,9 @@ __device__ __forceinline__ float4 vsel(bool c, float4 a, float4 b) {
 // -- or the next row's first batch -- are loaded while the current batch's
 // gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
 // evict-first so L2 keeps the gathered rows of Q(r-1).
-template <typename T, int G, int VPL, int MODE, int PEAK>
+template <typename T, int G, int VPL, int MODE, int PEAK, bool STAGED = false>
 __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_step(const StepParams P) {
+    extern __shared__ __align__(128) unsigned char k1_dyn_smem[];
     typedef typename Vec<T>::type VT;
     constexpr int W = Vec<T>::W;
     constexpr int RPW = 32 / G;  // rows per warp
@@ -305,18 +333,47 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         mya = __ldcs(vals + beg + gl);
     }
 
-    // gathers of the first D-1 entries of the current batch, carried across batches
+    // Gathers of the first D-1 entries of the current batch are carried across
+    // batches.  Register variant: D-deep rotating register buffer.  Staged
+    // variant (STAGED): lane 0 of each group issues one TMA bulk copy of the
+    // neighbour's row tile into a warp-private S-stage shared-memory ring; the
+    // group waits on the stage's mbarrier and consumes it from shared memory.
     constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (sizeof(T) == 8 ? 4 : 2);
-    constexpr int D = (DEPTH < B) ? DEPTH : B;
+    constexpr int D = STAGED ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
     static_assert(B % D == 0, "pipeline depth must divide the batch width");
-    VT buf[D][VPL];
-#pragma unroll
-    for (int e = 0; e < D - 1; ++e) {
-        const int j = __shfl_sync(0xFFFFFFFFu, myj, e, G);
-        const VT *x = ycur + (int64_t)j * P.ldv;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) buf[e][k] = ld_gather_if(x + k * G, valid[k] && e < end - beg);
+    VT buf[STAGED ? 1 : D][VPL];
+    uint64_t *bars = nullptr;
+    VT *ring = nullptr;
+    unsigned phase = 0u;  // staged: bit s = parity to wait for on stage s
+    const VT *ybase = (const VT *)P.ycur + P.v0;
+    const unsigned row_bytes = (unsigned)P.nvt * 16u;
+    if constexpr (STAGED) {
+        unsigned char *wb = k1_dyn_smem + P.smem_base +
+                            (size_t)(threadIdx.x >> 5) * (128 + (size_t)D * RPW * row_bytes);
+        bars = reinterpret_cast<uint64_t *>(wb);
+        ring = reinterpret_cast<VT *>(wb + 128);
+        if (lane < D) mbar_init(bars + lane, RPW);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
     }
+    auto issue = [&](int slot, int j, bool ok) {
+        if constexpr (STAGED) {
+            if (gl == 0) {
+                if (ok) {
+                    mbar_arrive_tx(bars + slot, row_bytes);
+                    tma_row(ring + ((size_t)slot * RPW + grp) * P.nvt, ybase + (int64_t)j * P.ldv, row_bytes, bars + slot);
+                } else {
+                    mbar_arrive(bars + slot);
+                }
+            }
+        } else {
+            const VT *x = ycur + (int64_t)j * P.ldv;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) buf[slot][k] = ld_gather_if(x + k * G, valid[k] && ok);
+        }
+    };
+#pragma unroll
+    for (int e = 0; e < D - 1; ++e) issue(e, __shfl_sync(0xFFFFFFFFu, myj, e, G), e < end - beg);
 
     for (int64_t wbase = warp * RPW; wbase < P.n_rows; wbase += wstride) {  // warp-uniform
         const bool active = it < P.n_rows;
@@ -353,8 +410,8 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 }
             }
             const int cnt = len - b * B;  // entries of this batch for my row (may be <= 0)
-            // branch-free pipeline, D entries deep: step t issues the gathers of entry
-            // t+D-1 (spilling into the NEXT batch's first entries near the end, so no
+            // branch-free pipeline, D entries deep: step t issues entry t+D-1
+            // (spilling into the NEXT batch's first entries near the end, so no
             // batch or row-set epilogue starts with an empty pipeline) and consumes t
 #pragma unroll
             for (int t = 0; t < B; ++t) {
@@ -362,24 +419,28 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 const int j = (e < B) ? __shfl_sync(0xFFFFFFFFu, myj, e % B, G)
                                       : __shfl_sync(0xFFFFFFFFu, nj, e % B, G);
                 const bool more = (e < B) ? (e < cnt) : (e - B < ncnt);
-#if (K1_ABLATE & 2)
-                const VT *x = ycur + row * (int64_t)P.ldv;
-#else
-                const VT *x = ycur + (int64_t)j * P.ldv;
-#endif
-                if (D > 1) {
-#pragma unroll
-                    for (int k = 0; k < VPL; ++k) buf[e % D][k] = ld_gather_if(x + k * G, valid[k] && more);
-                }
-                // a padded step (t >= cnt) has a == 0 and a zero vector: acc + (+0) == acc
-                // exactly, because acc is never -0 (it starts at +0, as scipy's y does)
+                if (D > 1) issue(e % D, j, more);
                 const T a = __shfl_sync(0xFFFFFFFFu, mya, t, G);
-                if (D == 1) {
+                if (D == 1) issue(0, j, more);
+                if constexpr (STAGED) {
+                    const int slot = t % D;
+                    const unsigned par = (phase >> slot) & 1u;
+                    for (unsigned spins = 0; !mbar_try_wait(bars + slot, par);) {
+                        if (++spins > (1u << 26)) __trap();  // a lost copy must fail loudly, not hang
+                    }
+                    phase ^= 1u << slot;
+                    const VT *src = ring + ((size_t)slot * RPW + grp) * P.nvt + gl;
+                    const bool ok = t < cnt;  // padding steps were never copied: skip them
 #pragma unroll
-                    for (int k = 0; k < VPL; ++k) buf[0][k] = ld_gather_if(x + k * G, valid[k] && more);
+                    for (int k = 0; k < VPL; ++k)
+                        if (valid[k]) acc[k] = vsel(ok, vmadd(acc[k], a, src[k * G]), acc[k]);
+                    __syncwarp();  // the stage is re-issued D-1 steps later
+                } else {
+                    // a padded step (t >= cnt) has a == 0 and a zero vector: acc + (+0) == acc
+                    // exactly, because acc is never -0 (it starts at +0, as scipy's y does)
+#pragma unroll
+                    for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, buf[t % D][k]);
                 }
-#pragma unroll
-                for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, buf[t % D][k]);
             }
             if (b + 1 < nb_mine || b + 1 >= nb) {
                 myj = nj;
@@ -394,12 +455,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 mya = __ldcs(vals + beg2 + gl);
             }
 #pragma unroll
-            for (int e = 0; e < D - 1; ++e) {
-                const int j = __shfl_sync(0xFFFFFFFFu, myj, e, G);
-                const VT *x = ycur + (int64_t)j * P.ldv;
-#pragma unroll
-                for (int k = 0; k < VPL; ++k) buf[e][k] = ld_gather_if(x + k * G, valid[k] && e < end2 - beg2);
-            }
+            for (int e = 0; e < D - 1; ++e) issue(e, __shfl_sync(0xFFFFFFFFu, myj, e, G), e < end2 - beg2);
         }
 
         if (active) {
@@ -461,7 +517,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
 
     if (MODE == MODE_RECUR && P.peaks) {
         // per-chunk max over the block, then one atomic per chunk per block
-        extern __shared__ unsigned long long s_peak[];
+        unsigned long long *s_peak = reinterpret_cast<unsigned long long *>(k1_dyn_smem);
         const int last_chunk = (P.col0 + (P.v0 + P.nvt) * W - 1) >> 5;
         const int nch = last_chunk - first_chunk + 1;
         for (int c = threadIdx.x; c < nch; c += blockDim.x) s_peak[c] = 0ull;
