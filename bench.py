@@ -269,6 +269,7 @@ def _gather_columns(plan, dm, n, d, world, rank, local_rank, dtype):
     E = assemble_columns(local, world, d, dtype)
     torch.cuda.current_stream().synchronize()
     _lib.check(dm.lib.csemb_rownorm(dm.ctx.handle, E.data_ptr(), n, d, d, _lib.F64 if dtype == "f64" else _lib.F32))
+    dm.ctx.sync()  # E is torch-owned: finish the library-stream kernel before torch may recycle it
     return E
 
 
