@@ -1297,7 +1297,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     if (e == cudaSuccess) {
         // V /= ||V||_col  (engine.py:181)
         k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, nullptr, n, (int)k, ld, partial);
-        k_colfinish<<<(int)((k + 127) / 128), 128, 0, s>>>(partial, gy, (int)k, nullptr, inv);
+        k_colfinish<<<(int)((k * 32 + 255) / 256), 256, 0, s>>>(partial, gy, (int)k, nullptr, inv);
         k_colscale<T><<<gs, 256, 0, s>>>(V, V, inv, n, (int)k, ld);
         e = cudaGetLastError();
     }
@@ -1327,7 +1327,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
         if (e != cudaSuccess) break;
         // Rayleigh quotients and column norms (engine.py:185-187), then V = W / ||W|| (:191)
         k_colstats<T><<<dim3(gx, gy), dim3(32, 8), 0, s>>>(V, Wm, n, (int)k, ld, partial);
-        k_colfinish<<<(int)((k + 127) / 128), 128, 0, s>>>(partial, gy, (int)k, rq + (size_t)it * k, inv);
+        k_colfinish<<<(int)((k * 32 + 255) / 256), 256, 0, s>>>(partial, gy, (int)k, rq + (size_t)it * k, inv);
         k_colscale<T><<<gs, 256, 0, s>>>(V, Wm, inv, n, (int)k, ld);
         e = cudaGetLastError();
     }

@@ -582,7 +582,22 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
         VT acc[MS];
 #pragma unroll
         for (int k = 0; k < MS; ++k) acc[k] = vzero(VT());
-        for (int c = c0; c < c1; ++c) {
+        // chunk partials in chunk order; 8 chunks' loads in flight at a time
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {
+            VT x[8][MS];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int k = 0; k < MS; ++k)
+                    x[u][k] = valid[k] ? part[(int64_t)(c + u) * P.ldv + 32 * k] : vzero(VT());
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int k = 0; k < MS; ++k)
+                    if (valid[k]) acc[k] = vmadd(acc[k], (T)1, x[u][k]);
+        }
+        for (; c < c1; ++c) {
 #pragma unroll
             for (int k = 0; k < MS; ++k)
                 if (valid[k]) acc[k] = vmadd(acc[k], (T)1, part[(int64_t)c * P.ldv + 32 * k]);
@@ -779,18 +794,27 @@ __global__ void k_colstats(const T *__restrict__ V, const T *__restrict__ Wm, in
     }
 }
 
-// fixed-order sum of the partials: rq[c] = dot, inv[c] = 1/sqrt(sq) (0 if sq == 0)
+// fixed-order sum of the partials, one warp per column (lane-strided partial
+// sums, then a shuffle tree): rq[c] = dot, inv[c] = 1/sqrt(sq) (0 if sq == 0)
 __global__ void k_colfinish(const double *partial, int nparts, int k, double *rq, double *inv) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= k) return;
+    const int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= k) return;  // whole warps exit together
     double a = 0.0, b = 0.0;
-    for (int p = 0; p < nparts; ++p) {
+    for (int p = lane; p < nparts; p += 32) {
         a += partial[((int64_t)p * 2 + 0) * k + c];
         b += partial[((int64_t)p * 2 + 1) * k + c];
     }
-    if (rq) rq[c] = a;
-    const double nrm = sqrt(b);
-    inv[c] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if (lane == 0) {
+        if (rq) rq[c] = a;
+        const double nrm = sqrt(b);
+        inv[c] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    }
 }
 
 // dst[r,c] = src[r,c] * inv[c]  (dead columns become 0, like dropping them)

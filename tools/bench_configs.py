@@ -54,7 +54,7 @@ def run_embed(dm, coeffs, d, reps, dtype, normalize=True):
         plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7, normalize_rows=normalize)
         dm.ctx.sync()
         res.append(plan.timing())
-    tot, steps, launches = min(res[1:], key=lambda t: t[0])
+    tot, steps, launches = min(res[1:] or res, key=lambda t: t[0])
     L = len(coeffs) - 1
     return tot, steps / L, launches, plan  # K1 time per recurrence step (all its launches)
 
