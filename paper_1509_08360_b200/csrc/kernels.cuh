@@ -44,8 +44,15 @@ __device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0
 __device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // acc + a*x, separately rounded (fp64 strict) / fused (fp32)
+#ifndef K1_FMA64
+#define K1_FMA64 0  // 1: fused multiply-add in fp64 (not bit-identical to the reference; experiment)
+#endif
 __device__ __forceinline__ double2 vmadd(double2 acc, double a, double2 x) {
+#if K1_FMA64
+    return make_double2(fma(a, x.x, acc.x), fma(a, x.y, acc.y));
+#else
     return make_double2(__dadd_rn(acc.x, __dmul_rn(a, x.x)), __dadd_rn(acc.y, __dmul_rn(a, x.y)));
+#endif
 }
 __device__ __forceinline__ float4 vmadd(float4 acc, float a, float4 x) {
     return make_float4(fmaf(a, x.x, acc.x), fmaf(a, x.y, acc.y), fmaf(a, x.z, acc.z),

@@ -26,6 +26,7 @@ ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--graphs", default="band,sbm,random")
 ap.add_argument("--widths", default="80")
 ap.add_argument("--efold", type=int, default=None)
+ap.add_argument("--reverse", type=int, default=None)
 args = ap.parse_args()
 n = args.n
 
@@ -48,6 +49,8 @@ for name in args.graphs.split(","):
         plan = dm.plan(w)
         if args.efold:
             plan.set_option(_lib.OPT_E_FOLD, args.efold)
+        if args.reverse is not None:
+            plan.set_option(_lib.OPT_REVERSE_SWEEP, args.reverse)
         best = 1e9
         for _ in range(3):
             plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
