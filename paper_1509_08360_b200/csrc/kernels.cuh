@@ -176,40 +176,19 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #define K1_ABLATE 0  // timing experiments only (results are wrong when nonzero)
 #endif
 
-// Gathers of Q(r-1) rows.  GATHER_MODE 0: ld.global.nc (L1-allocating, 128-byte
-// line requests); 1: ld.global.nc.L1::no_allocate; 2: ld.global.cg (L2 only).
+// Gathers of Q(r-1) rows: ld.global.nc (read-only path, L1-allocating, 128-byte
+// line requests).  Measured on config 2: .cg / .nc.L1::no_allocate (L2 only)
+// and an L2::evict_last policy were not faster.
 #ifndef GATHER_MODE
-#define GATHER_MODE 0
+#define GATHER_MODE 0  // 1: ld.global.nc.L1::no_allocate, 2: ld.global.cg (experiments)
 #endif
-#if GATHER_MODE == 3
-#define GATHER_HINT 1
-#define GATHER_OP "ld.global.nc.L2::cache_hint"
-#elif GATHER_MODE == 1
+#if GATHER_MODE == 1
 #define GATHER_OP "ld.global.nc.L1::no_allocate"
 #elif GATHER_MODE == 2
 #define GATHER_OP "ld.global.cg"
 #else
 #define GATHER_OP "ld.global.nc"
 #endif
-#ifdef GATHER_HINT
-// L2 evict_last policy for gathered rows (streams stay evict-first)
-__device__ __forceinline__ uint64_t gather_policy() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ double2 ld_gather(const double2 *p) {
-    double2 v;
-    asm(GATHER_OP ".v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(gather_policy()));
-    return v;
-}
-__device__ __forceinline__ float4 ld_gather(const float4 *p) {
-    float4 v;
-    asm(GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(gather_policy()));
-    return v;
-}
-#else
 __device__ __forceinline__ double2 ld_gather(const double2 *p) {
     double2 v;
     asm(GATHER_OP ".v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
@@ -220,7 +199,7 @@ __device__ __forceinline__ float4 ld_gather(const float4 *p) {
     asm(GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
     return v;
 }
-#endif
+
 // Predicated gathers (branch-free: a not-taken load neither issues traffic nor
 // splits the unrolled entry loop into separate basic blocks, so the scheduler
 // can keep several entries' gathers in flight).

@@ -565,3 +565,46 @@ class TestEFold:
         ref, _, _ = O.apply_expansion(O.CSR.of(S), th, om, n_stages=3)
         got = pb.device_matrix(S).plan(16).apply(th, 3, om)
         assert np.array_equal(got, ref)
+
+
+class TestABIErrors:
+    """Every invalid request returns CSEMB_ERR_INVALID (ValueError), never a crash."""
+
+    def test_plan_argument_checks(self):
+        S = graphs.sbm(300, 3, 6.0, 2.0, seed=1)
+        dm = pb.DeviceMatrix(S)
+        plan = dm.plan(8)
+        th = np.ones(4)
+        with pytest.raises(ValueError, match="col0"):
+            plan.run(th, 1, omega_kind=1, col0=1, d_global=16)
+        with pytest.raises(ValueError):
+            plan.run(th, 1, omega_kind=1, col0=0, d_global=4)
+        with pytest.raises(ValueError, match="finite"):
+            plan.run(np.array([1.0, np.nan]), 1, omega_kind=1)
+        with pytest.raises(ValueError):
+            plan.run(th, 0, omega_kind=1)
+        with pytest.raises(ValueError):
+            plan.run(th, 1, omega_kind=0)  # GIVEN without a block
+        with pytest.raises(ValueError, match="begin"):
+            plan.step(1)
+        with pytest.raises(ValueError):
+            plan.set_option(pb._lib.OPT_E_FOLD, 7)
+        with pytest.raises(ValueError):
+            plan.set_option(99, 1)
+        with pytest.raises(ValueError):
+            dm.scale(0.0)
+        dm.close()
+
+    def test_matrix_checks(self):
+        S = graphs.sbm(200, 2, 5.0, 1.0, seed=2)
+        bad = pb.SparseMatrix(S.n_rows, 10, S.row_offsets, S.col_indices % 10, S.values, check=False)
+        with pytest.raises(ValueError, match="column index"):
+            pb.DeviceMatrix(pb.SparseMatrix(S.n_rows, 5, S.row_offsets, S.col_indices, S.values, check=False))
+        dm = pb.DeviceMatrix(bad)  # valid columns (mod 10) but a non-square matrix
+        with pytest.raises(ValueError, match="square"):
+            dm.plan(4).run(np.ones(3), 1, omega_kind=1)
+        dm.close()
+        sq = pb.DeviceMatrix(S)
+        with pytest.raises(ValueError):
+            sq.plan(4).partition(0, S.n_rows + 5, 0)
+        sq.close()
