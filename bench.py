@@ -26,7 +26,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -176,14 +175,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        k1_ms = []
         with ClockSampler(local_rank) as clk:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(ext)
             for _ in range(args.steps):
                 one_step()
-                if world == 1:
-                    pass
             ev1.record(ext)
             dm.ctx.sync()
             torch.cuda.synchronize()

@@ -639,7 +639,12 @@ extern "C" int csemb_matrix_upload_device(csemb_ctx *c, int64_t n_rows, int64_t 
         return fail(CSEMB_ERR_INVALID, hbad ? "column index out of range" : "row_offsets must run from 0 to nnz");
     }
     m->rowptr_host.resize((size_t)n_rows + 1);
-    CK(cudaMemcpy(m->rowptr_host.data(), m->rowptr, 8 * ((size_t)n_rows + 1), cudaMemcpyDeviceToHost));
+    e = cudaMemcpy(m->rowptr_host.data(), m->rowptr, 8 * ((size_t)n_rows + 1), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mat_free(m);
+        return fail(CSEMB_ERR_CUDA, "device matrix upload: %s", cudaGetErrorString(e));
+    }
     for (int64_t i = 0; i < n_rows; ++i)
         if (m->rowptr_host[i + 1] < m->rowptr_host[i]) {
             mat_free(m);

@@ -506,7 +506,6 @@ def fast_embed_general(A, f, cfg: EmbedConfig, *, quadrature=None, n_workers: in
     emb = fast_embed_cascaded(S, odd_extension(f), cfg, None, quadrature=quadrature, counter=counter,
                               dtype=dtype, device=device, normalize_rows=normalize_rows,
                               omega_kind=omega_kind)
-    emb.provenance["function"] = _describe(odd_extension(f))
     base = dict(emb.provenance)
     rows = EmbeddingMatrix(values=emb.values[n:], row_labels=np.arange(m, dtype=np.int64),
                            provenance={**base, "side": "rows"})

@@ -608,3 +608,76 @@ class TestABIErrors:
         with pytest.raises(ValueError):
             sq.plan(4).partition(0, S.n_rows + 5, 0)
         sq.close()
+
+
+class TestReferenceSuiteOnDevice:
+    """The reference suite's numerical criteria, run through the device path."""
+
+    def test_linearity_in_function(self):  # tests/test_engine.py:132-150
+        rng = np.random.default_rng(8)
+        n = 40
+        a = rng.standard_normal((n, n))
+        a = 0.5 * (a + a.T)
+        a *= 0.95 / np.linalg.norm(a, 2)
+        S = pb.SparseMatrix.from_dense(a)
+        om = O.sample_projection(n, 5, 8)
+        f, g = pb.indicator_above(0.2), pb.constant(1.0)
+        quad = pb.QuadratureSpec(breakpoints=(0.2,))
+        combo = lambda x: 0.6 * np.asarray(f(x)) - 1.1 * np.asarray(g(x))  # noqa: E731
+        lhs = pb.fast_embed_eig(S, combo, 25, om, quadrature=quad).values
+        rhs = 0.6 * pb.fast_embed_eig(S, f, 25, om, quadrature=quad).values - 1.1 * pb.fast_embed_eig(
+            S, g, 25, om, quadrature=quad).values
+        assert np.linalg.norm(lhs - rhs) <= 1e-12 * max(1.0, np.linalg.norm(rhs))
+
+    def test_a9_norm_estimator_band(self):  # tests/test_acceptance.py:357-386
+        rng = np.random.default_rng(99)
+        for i in range(50):
+            lam = np.concatenate([[1.0 if i % 2 else -1.0], rng.uniform(-0.85, 0.85, 199)])
+            q, _ = np.linalg.qr(rng.standard_normal((200, 200)))
+            dense = (q * lam) @ q.T
+            est = pb.estimate_spectral_norm(pb.SparseMatrix.from_dense(dense), pb.EmbedConfig(L=1, d=1, seed=1000 + i))
+            assert 0.99 <= est / np.abs(lam).max() <= 1.01 + 1e-12
+
+    def test_a1_polynomial_exactness(self):  # tests/test_acceptance.py:36-56
+        rng = np.random.default_rng(101)
+        n = 100
+        dense = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.05)
+        dense = 0.5 * (dense + dense.T)
+        dense /= np.linalg.norm(dense, 2)
+        om = O.sample_projection(n, 16, 11)
+        emb = pb.fast_embed_eig(pb.SparseMatrix.from_dense(dense), lambda x: 0.3 + 0.5 * x - 0.2 * x**3, 3, om)
+        oracle = 0.3 * om + 0.5 * (dense @ om) - 0.2 * np.linalg.matrix_power(dense, 3) @ om
+        assert np.linalg.norm(emb.values - oracle) / np.linalg.norm(oracle) <= 1e-10
+
+
+def test_fuzz_random_csr_bit_exact():
+    """Random CSR shapes (empty rows, heavy rows, odd widths) vs the oracle."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=40, deadline=None)
+    @given(n=st.integers(1, 400), density=st.floats(0.0, 0.2), heavy=st.booleans(), d=st.integers(1, 70),
+           L=st.integers(0, 9), seed=st.integers(0, 2**31), f32=st.booleans())
+    def check(n, density, heavy, d, L, seed, f32):
+        rng = np.random.default_rng(seed)
+        a = rng.standard_normal((n, n)) * (rng.random((n, n)) < density)
+        if heavy and n > 2:
+            a[n // 2, :] = rng.standard_normal(n)
+        a = 0.5 * (a + a.T)
+        nrm = np.linalg.norm(a, 2) if a.any() else 1.0
+        S = pb.SparseMatrix.from_dense(a / (1.05 * nrm))
+        om = O.sample_projection(n, d, seed % 1000)
+        th = rng.standard_normal(L + 1) * 0.5
+        ref, _, _ = O.run_stage(O.CSR.of(S), th, om)
+        dm = pb.device_matrix(S, "float32" if f32 else "float64")
+        plan = dm.plan(d)
+        plan.set_load_balance(split_threshold=64 if heavy else 4096)
+        got = plan.apply(th, 1, om)
+        if f32:
+            assert rel(got, ref) <= 1e-4 or np.linalg.norm(ref) < 1e-6
+        elif heavy and n > 64:
+            assert rel(got, ref) <= 1e-13 or np.linalg.norm(ref) == 0
+        else:
+            assert np.array_equal(got, ref)
+
+    check()
