@@ -52,6 +52,7 @@ extern "C" {
 typedef struct csemb_ctx csemb_ctx;
 typedef struct csemb_mat csemb_mat;
 typedef struct csemb_plan csemb_plan;
+typedef struct csemb_kmeans csemb_kmeans;
 
 const char *csemb_last_error(void);
 int csemb_abi_version(void);
@@ -183,6 +184,54 @@ int csemb_rownorm(csemb_ctx *ctx, void *E_dev, int64_t n, int64_t d, int64_t ld,
  * max over iterations of max|Rayleigh quotient| times `safety`.  */
 int csemb_spectral_norm(csemb_mat *m, int iters, int64_t k, const double *v0_host,
                         uint64_t seed, double safety, double *out);
+
+/* ---- downstream consumers of an embedding -------------
+ * Reference: cluster.py (k-means, modularity) and oracle.py:88-119 (sampled
+ * pair correlations).  Row squared norms follow numpy's pairwise order and
+ * centroid sums follow np.add.at's row order (bit-identical); dot products are
+ * fused in a fixed order where the reference uses BLAS (agreement to ulps).  */
+
+/* _pair_correlations (oracle.py:88-96): cos_out[p] = <E_a, E_b> / (|E_a| |E_b|)
+ * for pairs_host[2p], pairs_host[2p+1]; zero-norm pairs give 0 and
+ * zero_out[p] = 1 (zero_out may be NULL).  E: n x ld block, in device memory
+ * (on_device != 0, e.g. csemb_plan_output) or on the host (uploaded).  */
+int csemb_pair_cosines(csemb_ctx *ctx, const void *E, int dtype, int on_device, int64_t n, int64_t d,
+                       int64_t ld, const int64_t *pairs_host, int64_t n_pairs, double *cos_out,
+                       uint8_t *zero_out);
+
+/* k-means (cluster.py:59-107).  The caller runs the reference's loop and owns
+ * the random stream (numpy Generator); the handle holds an f64 copy of X and
+ * the device state.  Steps:
+ *   seed(k, row, &total)   centroid k = X[row]; closest = d2 (k == 0) or
+ *                          min(closest, d2); total = sum(closest)   (:46-55)
+ *   pick(u, &row)          rng.choice(n, p=closest/total) given u = rng.random()
+ *                          (first i with cumsum(p)[i] / cumsum(p)[-1] > u)
+ *   assign(&inertia, &changed, counts)  labels/mindist of the current
+ *                          centroids, sum(mindist), #labels changed, counts (:74-82)
+ *   reseed(c, &row)        empty cluster c: row = argmax(avail); centroid c =
+ *                          X[row]; new_labels[row] = c; avail[row] = -1 (:84-90)
+ *   commit(update)         labels = new_labels; update != 0 also recomputes the
+ *                          centroids as per-cluster means (:95-100)  */
+int csemb_kmeans_create(csemb_ctx *ctx, const void *X, int dtype, int on_device, int64_t n, int64_t d,
+                        int64_t ld, int K, csemb_kmeans **out);
+int csemb_kmeans_destroy(csemb_kmeans *km);
+int csemb_kmeans_seed(csemb_kmeans *km, int k, int64_t row, double *total);
+int csemb_kmeans_pick(csemb_kmeans *km, double u, int64_t *row);
+int csemb_kmeans_assign(csemb_kmeans *km, double *inertia, int64_t *changed, int64_t *counts);
+int csemb_kmeans_reseed(csemb_kmeans *km, int c, int64_t *row);
+int csemb_kmeans_commit(csemb_kmeans *km, int update_centroids);
+int csemb_kmeans_download(csemb_kmeans *km, int64_t *labels_host, double *centroids_host);
+int csemb_kmeans_set_centroids(csemb_kmeans *km, const double *centroids_host);
+int csemb_kmeans_reset(csemb_kmeans *km); /* labels back to -1 for a new restart (same rows) */
+const int32_t *csemb_kmeans_labels(csemb_kmeans *km); /* device, n int32 (current labels) */
+
+/* modularity (cluster.py:110-128) counts over the matrix's CSR pattern, which
+ * must be the simple undirected graph (each edge stored both ways, no
+ * diagonal -- e.g. a normalized_adjacency).  intra[c] = edges inside cluster c,
+ * degsum[c] = sum of degrees in c, for labels in [0, k).  The caller forms
+ * Q = sum(intra/m - (degsum/2m)^2) with m = nnz/2 exactly as the reference.  */
+int csemb_modularity_counts(csemb_mat *m, const int32_t *labels, int on_device, int64_t k, int64_t *intra,
+                            int64_t *degsum);
 
 #ifdef __cplusplus
 }

@@ -248,8 +248,78 @@ def sample_pairs(n: int, n_pairs: int, seed: int) -> np.ndarray:
     return np.stack([codes // np.uint64(n), codes % np.uint64(n)], axis=1).astype(np.int64)
 
 
+# -- downstream consumers (reference cluster.py) ------------------------------
+
+
+def _sqdist(X: np.ndarray, Cn: np.ndarray) -> np.ndarray:
+    """cluster._sq_distances (cluster.py:34-40): max(|x|^2 + |c|^2 - 2 x.c, 0)."""
+    g = X @ Cn.T
+    return np.maximum(np.sum(X * X, axis=1)[:, None] + np.sum(Cn * Cn, axis=1)[None, :] - 2.0 * g, 0.0)
+
+
+def kmeans(X: np.ndarray, K: int, max_iters: int = 100, seed: int = 0):
+    """cluster.kmeans (cluster.py:43-107): k-means++ seeding then Lloyd
+    iterations; returns (labels, inertia_history).  Same Generator draws:
+    integers(n) for the first centroid and the zero-total branch, choice(n, p)
+    for weighted picks; empty clusters take the farthest remaining point and
+    skip the mean update; stop when labels repeat."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    if not 1 <= K <= n:
+        raise ValueError(f"K={K} must lie in [1, n_rows={n}]")
+    rng = np.random.default_rng(seed)
+    cent = np.empty((K, X.shape[1]))
+    cent[0] = X[rng.integers(n)]
+    near = _sqdist(X, cent[:1])[:, 0]
+    for k in range(1, K):
+        tot = near.sum()
+        row = int(rng.integers(n)) if tot <= 0.0 else int(rng.choice(n, p=near / tot))
+        cent[k] = X[row]
+        near = np.minimum(near, _sqdist(X, cent[k:k + 1])[:, 0])
+    labels = np.full(n, -1, dtype=np.int64)
+    hist: list[float] = []
+    for _ in range(max_iters):
+        d2 = _sqdist(X, cent)
+        new = np.argmin(d2, axis=1).astype(np.int64)
+        best = d2[np.arange(n), new]
+        hist.append(float(best.sum()))
+        sizes = np.bincount(new, minlength=K)
+        if (sizes == 0).any():
+            free = best.copy()
+            for c in np.flatnonzero(sizes == 0):
+                far = int(np.argmax(free))
+                cent[c], new[far], free[far] = X[far], c, -1.0
+            labels = new
+            continue
+        done = np.array_equal(new, labels)
+        labels = new
+        if done:
+            break
+        acc = np.zeros_like(cent)
+        np.add.at(acc, labels, X)
+        cent = acc / np.bincount(labels, minlength=K)[:, None]
+    return labels, hist
+
+
+def modularity(edges: np.ndarray, labels: np.ndarray) -> tuple[float, int]:
+    """cluster.modularity (cluster.py:110-128) -> (Q, m) over the simple
+    undirected graph of `edges` (loops dropped, duplicates merged)."""
+    e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    e = e[e[:, 0] != e[:, 1]]
+    und = np.unique(np.sort(e, axis=1), axis=0)
+    m = len(und)
+    lab = np.asarray(labels, dtype=np.int64)
+    k = int(lab.max()) + 1
+    lu, lv = lab[und[:, 0]], lab[und[:, 1]]
+    intra = np.bincount(lu[lu == lv], minlength=k)
+    deg = np.bincount(und.ravel(), minlength=len(lab))
+    degsum = np.bincount(lab, weights=deg, minlength=k)
+    return float(np.sum(intra / m - (degsum / (2.0 * m)) ** 2)), m
+
+
 __all__ = [
     "CSR", "build", "lib", "set_threads", "num_threads", "fold_seed", "sample_projection",
     "np_sample_projection", "spmm", "run_stage", "apply_expansion", "spectral_norm",
-    "norm_start_block", "row_normalize", "pair_cosines", "sample_pairs", "NORM_SEED_TAG",
+    "norm_start_block", "row_normalize", "pair_cosines", "sample_pairs", "NORM_SEED_TAG", "kmeans",
+    "modularity",
 ]

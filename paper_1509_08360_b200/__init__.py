@@ -6,7 +6,9 @@ SpMM-recurrence kernel (sm_100a), behind the reference's public signatures.
 Host-side pieces (coefficients, spectral functions, CSR container, input
 builders) mirror the reference; the recurrence, the projection block, the
 power-iteration norm estimate and the row normalisation run on the device
-through the C ABI in include/csemb_cuda.h.
+through the C ABI in include/csemb_cuda.h.  The embedding's downstream
+consumers (k-means, modularity, sampled-pair distortion: `cluster`,
+`distortion`) run on the device as well.
 """
 
 from .engine import (
@@ -29,6 +31,18 @@ from .engine import (
     norm_start_block,
     sample_projection,
 )
+from .cluster import (
+    ClusterAssignment,
+    ClusterExperiment,
+    DeviceKMeans,
+    DeviceRows,
+    ModularityScore,
+    cluster_experiment,
+    kmeans,
+    modularity,
+    plan_rows,
+)
+from .distortion import DistortionReport, distortion_percentiles, pair_correlations, sample_pairs
 from .errors import CsembError, CudaUnavailableError, DivergenceError, InputFormatError
 from .functions import (
     SpectralFunction,
@@ -65,4 +79,8 @@ __all__ = [
     "legendre_coefficients", "legendre_eval", "legendre_table", "norm_start_block",
     "normalized_adjacency", "odd_extension", "parse_function", "remapped", "root_function",
     "sample_projection", "scale_values", "simple_edges", "tabulated",
+    # downstream consumers (cluster.py, oracle.py:88-186)
+    "ClusterAssignment", "ClusterExperiment", "DeviceKMeans", "DeviceRows", "DistortionReport",
+    "ModularityScore", "cluster_experiment", "distortion_percentiles", "kmeans", "modularity",
+    "pair_correlations", "plan_rows", "sample_pairs",
 ]

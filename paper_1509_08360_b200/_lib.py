@@ -73,6 +73,20 @@ SIGNATURES = {
     "csemb_sample_projection": (_int, [_p, _i64, _i64, _u64, _i64, _i64, _int, _p]),
     "csemb_rownorm": (_int, [_p, _p, _i64, _i64, _i64, _int]),
     "csemb_spectral_norm": (_int, [_p, _int, _i64, _p, _u64, _dbl, _pd]),
+    # downstream consumers (cluster.py, oracle.py:88-119)
+    "csemb_pair_cosines": (_int, [_p, _p, _int, _int, _i64, _i64, _i64, _p, _i64, _p, _p]),
+    "csemb_kmeans_create": (_int, [_p, _p, _int, _int, _i64, _i64, _i64, _int, _pp]),
+    "csemb_kmeans_destroy": (_int, [_p]),
+    "csemb_kmeans_seed": (_int, [_p, _int, _i64, _pd]),
+    "csemb_kmeans_pick": (_int, [_p, _dbl, _pi64]),
+    "csemb_kmeans_assign": (_int, [_p, _pd, _pi64, _p]),
+    "csemb_kmeans_reseed": (_int, [_p, _int, _pi64]),
+    "csemb_kmeans_commit": (_int, [_p, _int]),
+    "csemb_kmeans_download": (_int, [_p, _p, _p]),
+    "csemb_kmeans_set_centroids": (_int, [_p, _p]),
+    "csemb_kmeans_reset": (_int, [_p]),
+    "csemb_kmeans_labels": (_p, [_p]),
+    "csemb_modularity_counts": (_int, [_p, _p, _int, _i64, _p, _p]),
 }
 
 _lock = threading.Lock()

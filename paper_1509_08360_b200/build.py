@@ -14,8 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcsemb_cuda.so")
-SOURCES = [os.path.join(HERE, "csrc", "csemb_cuda.cu")]
-DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "csemb_cuda.h")]
+SOURCES = [os.path.join(HERE, "csrc", "csemb_cuda.cu"), os.path.join(HERE, "csrc", "downstream.cu")]
+DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "csemb_cuda.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -15,8 +15,8 @@
 #include <unordered_map>
 #include <vector>
 
-#include "../../include/csemb_cuda.h"
 #include "kernels.cuh"
+#include "runtime.h"
 
 using namespace csemb;
 
@@ -25,7 +25,7 @@ using namespace csemb;
 // ---------------------------------------------------------------------------
 static thread_local std::string g_err;
 
-static int fail(int code, const char *fmt, ...) {
+int fail(int code, const char *fmt, ...) {
     char buf[1024];
     va_list ap;
     va_start(ap, fmt);
@@ -34,57 +34,6 @@ static int fail(int code, const char *fmt, ...) {
     g_err = buf;
     return code;
 }
-
-#define CK(...)                                                                            \
-    do {                                                                                   \
-        cudaError_t e_ = (__VA_ARGS__);                                                              \
-        if (e_ != cudaSuccess) {                                                           \
-            cudaGetLastError();                                                            \
-            return fail(e_ == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, \
-                        "%s failed: %s (%s:%d)", #__VA_ARGS__, cudaGetErrorString(e_), __FILE__,     \
-                        __LINE__);                                                         \
-        }                                                                                  \
-    } while (0)
-
-// ---------------------------------------------------------------------------
-// handles
-// ---------------------------------------------------------------------------
-struct csemb_ctx {
-    int device = 0;
-    int sm_count = 0;
-    cudaStream_t stream = nullptr;
-    std::mutex mu;
-};
-
-// Load-balance schedule of a matrix for one group width G (see K1c in kernels.cuh):
-// rows longer than `threshold` are cut into chunks of `chunk` entries (heavy);
-// the other rows are swept in natural order or, when their lengths are skewed,
-// stably bucketed by batch count ceil(len/G) so a warp's rows need the same
-// number of batches.
-struct Schedule {
-    int G = 0;
-    int64_t threshold = 0;
-    int order = 0;
-    int *perm = nullptr;  // light rows (null: natural order, no heavy rows)
-    int64_t n_light = 0;
-    int64_t *cbeg = nullptr, *cend = nullptr;  // heavy-row chunk entry ranges
-    int64_t n_chunks = 0;
-    int *hrows = nullptr, *hoff = nullptr;     // heavy rows and their chunk offsets
-    int n_heavy = 0;
-    int *corder = nullptr;  // chunk execution order: by first column, so concurrently
-                            // running chunks gather neighbouring rows (L2 reuse)
-};
-
-struct csemb_mat {
-    csemb_ctx *ctx = nullptr;
-    int64_t n_rows = 0, n_cols = 0, nnz = 0;
-    int dtype = CSEMB_F64;
-    int64_t *rowptr = nullptr;
-    int *cols = nullptr;
-    void *vals = nullptr;
-    std::vector<int64_t> rowptr_host;
-    std::vector<Schedule *> schedules;
-};
 
 struct csemb_plan {
     csemb_mat *m = nullptr;
@@ -131,10 +80,10 @@ static void sched_free(Schedule *sc) {
     delete sc;
 }
 
-static size_t dsize(int dtype) { return dtype == CSEMB_F32 ? 4 : 8; }
+size_t dsize(int dtype) { return dtype == CSEMB_F32 ? 4 : 8; }
 static int vec_w(int dtype) { return dtype == CSEMB_F32 ? 4 : 2; }
 
-static int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8) {
+int grid_for(int64_t work_items, int threads, int sm_count, int per_sm) {
     int64_t g = (work_items + threads - 1) / threads;
     int64_t cap = (int64_t)sm_count * per_sm;
     if (g > cap) g = cap;
@@ -148,8 +97,8 @@ static int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 
 static std::mutex g_occ_mu;
 static std::unordered_map<const void *, int> g_occ;
 
-// Staged (TMA bulk-copy) K1 variant for groups of >= 8 lanes; CSEMB_K1_TMA=0/1
-// overrides the default.
+// Staged K1 variants for groups of >= 8 lanes (CSEMB_K1_TMA): 1 = TMA bulk copies
+// into per-warp mbarrier rings, 2 = per-lane cp.async rings; 0 (default) = registers.
 static int use_tma() {
     static int on = [] {
         const char *e = getenv("CSEMB_K1_TMA");
@@ -158,7 +107,7 @@ static int use_tma() {
     return on;
 }
 
-template <typename T, int G, int VPL, int MODE, int PEAK, bool STAGED>
+template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED>
 static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count) {
     const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK, STAGED>;
     const int threads = 256;
@@ -171,7 +120,10 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
         constexpr int RPW = 32 / G;
         constexpr int S = K1T_STAGES < G ? K1T_STAGES : G;
         P.smem_base = (int)((smem + 127) / 128 * 128);
-        smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
+        if (STAGED == 1)
+            smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
+        else
+            smem = P.smem_base + (size_t)S * threads * VPL * 16;
         max_smem = smem;
     }
     int per_sm;
@@ -198,9 +150,10 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
 template <typename T, int G, int VPL, int MODE, int PEAK>
 static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
     if constexpr (G >= 8) {
-        if (use_tma()) return run_step_t<T, G, VPL, MODE, PEAK, true>(P, s, sm_count);
+        if (use_tma() == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
+        if (use_tma() == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
     }
-    return run_step_t<T, G, VPL, MODE, PEAK, false>(P, s, sm_count);
+    return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
 }
 
 // VPL instantiations: 1..3 for G == 1, 2..3 for wider groups (more vectors per

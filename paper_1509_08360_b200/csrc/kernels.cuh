@@ -242,6 +242,15 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, unsigned parity) {
                  : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     return ok != 0;
 }
+// per-lane 16-byte async copy (LDGSTS); src_bytes 0 zero-fills without reading global
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // one neighbour-row tile (global -> shared), completion counted on `bar`
 __device__ __forceinline__ void tma_row(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -259,7 +268,7 @@ __device__ __forceinline__ void tma_row(void *dst, const void *src, unsigned byt
 // -- or the next row's first batch -- are loaded while the current batch's
 // gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
 // evict-first so L2 keeps the gathered rows of Q(r-1).
-template <typename T, int G, int VPL, int MODE, int PEAK, bool STAGED = false>
+template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED = 0>
 __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_step(const StepParams P) {
     extern __shared__ __align__(128) unsigned char k1_dyn_smem[];
     typedef typename Vec<T>::type VT;
@@ -326,6 +335,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     // group waits on the stage's mbarrier and consumes it from shared memory.
     constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (sizeof(T) == 8 ? 4 : 2);
     constexpr int D = STAGED ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
+    // STAGED == 2: per-lane ring of D entries x VPL 16-byte slots in shared memory
+    VT *lring = nullptr;
+    if constexpr (STAGED == 2)
+        lring = reinterpret_cast<VT *>(k1_dyn_smem + P.smem_base) + (size_t)threadIdx.x * VPL;
     static_assert(B % D == 0, "pipeline depth must divide the batch width");
     VT buf[STAGED ? 1 : D][VPL];
     uint64_t *bars = nullptr;
@@ -333,7 +346,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     unsigned phase = 0u;  // staged: bit s = parity to wait for on stage s
     const VT *ybase = (const VT *)P.ycur + P.v0;
     const unsigned row_bytes = (unsigned)P.nvt * 16u;
-    if constexpr (STAGED) {
+    if constexpr (STAGED == 1) {
         unsigned char *wb = k1_dyn_smem + P.smem_base +
                             (size_t)(threadIdx.x >> 5) * (128 + (size_t)D * RPW * row_bytes);
         bars = reinterpret_cast<uint64_t *>(wb);
@@ -343,7 +356,13 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         __syncwarp();
     }
     auto issue = [&](int slot, int j, bool ok) {
-        if constexpr (STAGED) {
+        if constexpr (STAGED == 2) {
+            const VT *x = ycur + (int64_t)j * P.ldv;
+            VT *dst = lring + (size_t)slot * blockDim.x * VPL;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) cp_async16(dst + k, x + k * G, (valid[k] && ok) ? 16 : 0);
+            cp_async_commit();
+        } else if constexpr (STAGED == 1) {
             if (gl == 0) {
                 if (ok) {
                     mbar_arrive_tx(bars + slot, row_bytes);
@@ -408,7 +427,13 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 if (D > 1) issue(e % D, j, more);
                 const T a = __shfl_sync(0xFFFFFFFFu, mya, t, G);
                 if (D == 1) issue(0, j, more);
-                if constexpr (STAGED) {
+                if constexpr (STAGED == 2) {
+                    cp_async_wait<D - 1>();  // entry t has landed (this lane's own copies)
+                    const VT *src = lring + (size_t)(t % D) * blockDim.x * VPL;
+                    // padding steps were zero-filled and a == 0: acc + (+0) == acc exactly
+#pragma unroll
+                    for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, src[k]);
+                } else if constexpr (STAGED == 1) {
                     const int slot = t % D;
                     const unsigned par = (phase >> slot) & 1u;
                     for (unsigned spins = 0; !mbar_try_wait(bars + slot, par);) {
@@ -501,6 +526,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         end = end2;
     }
 
+    if constexpr (STAGED == 2) cp_async_wait<0>();
     if (MODE == MODE_RECUR && P.peaks) {
         // per-chunk max over the block, then one atomic per chunk per block
         unsigned long long *s_peak = reinterpret_cast<unsigned long long *>(k1_dyn_smem);

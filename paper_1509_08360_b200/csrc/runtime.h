@@ -1,0 +1,72 @@
+// runtime.h -- handle structs and error plumbing shared by the C-ABI translation
+// units (csemb_cuda.cu: recurrence, projection, norm; downstream.cu: pair cosines,
+// k-means, modularity).  Internal: not part of include/csemb_cuda.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/csemb_cuda.h"
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+#define CSEMB_INTERNAL __attribute__((visibility("hidden")))
+
+// sets the thread-local csemb_last_error() text and returns `code`
+CSEMB_INTERNAL int fail(int code, const char *fmt, ...);
+
+#define CK(...)                                                                            \
+    do {                                                                                   \
+        cudaError_t e_ = (__VA_ARGS__);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            cudaGetLastError();                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, \
+                        "%s failed: %s (%s:%d)", #__VA_ARGS__, cudaGetErrorString(e_), __FILE__,     \
+                        __LINE__);                                                         \
+        }                                                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct csemb_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+};
+
+// Load-balance schedule of a matrix for one group width G (see K1c in kernels.cuh):
+// rows longer than `threshold` are cut into chunks of `chunk` entries (heavy);
+// the other rows are swept in natural order or, when their lengths are skewed,
+// stably bucketed by batch count ceil(len/G) so a warp's rows need the same
+// number of batches.
+struct Schedule {
+    int G = 0;
+    int64_t threshold = 0;
+    int order = 0;
+    int *perm = nullptr;  // light rows (null: natural order, no heavy rows)
+    int64_t n_light = 0;
+    int64_t *cbeg = nullptr, *cend = nullptr;  // heavy-row chunk entry ranges
+    int64_t n_chunks = 0;
+    int *hrows = nullptr, *hoff = nullptr;     // heavy rows and their chunk offsets
+    int n_heavy = 0;
+    int *corder = nullptr;  // chunk execution order: by first column, so concurrently
+                            // running chunks gather neighbouring rows (L2 reuse)
+};
+
+struct csemb_mat {
+    csemb_ctx *ctx = nullptr;
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;
+    int dtype = CSEMB_F64;
+    int64_t *rowptr = nullptr;
+    int *cols = nullptr;
+    void *vals = nullptr;
+    std::vector<int64_t> rowptr_host;
+    std::vector<Schedule *> schedules;
+};
+
+CSEMB_INTERNAL size_t dsize(int dtype);
+CSEMB_INTERNAL int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8);

@@ -1,0 +1,196 @@
+"""Sampled-pair correlation distortion with the pair work on the device
+(reference oracle.py:88-275; SURVEY 8(d) parity harness and 8(f) rank 4).
+
+``pair_correlations`` is ``_pair_correlations`` (oracle.py:88-96) on the GPU:
+one K5 launch (csemb_pair_cosines) for any number of pairs, on a host block or
+a device-resident embedding (DeviceRows, e.g. a plan's E -- no n x d
+download).  Norms follow numpy's pairwise order exactly; the dot products use
+the same order where the reference's einsum uses its own, so cosines agree to
+a few ulps.  Pair sampling, percentiles, binning and report writers are host
+code with the reference's exact numpy expressions.  The dense ground-truth
+embedding (oracle.exact_embedding, full eigh, capped at 3000 rows) stays with
+the caller: pass any row block (or object with ``.embedding``) as `exact`.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .cluster import DeviceRows
+from .engine import EmbeddingMatrix
+
+PERCENTILE_LEVELS = (1, 5, 25, 50, 75, 95, 99)
+DEFAULT_MAX_PAIRS = 100_000
+CALIBRATION_BIN_WIDTH = 0.1  # bins centred on -1.0, -0.9, ..., 1.0
+
+
+def sample_pairs(n: int, n_pairs: int | None, seed: int) -> np.ndarray:
+    """Uniform vertex pairs (i < j) without replacement, deterministic per seed
+    (oracle.py:99-119).  Same draw sequence as the reference: rounds of
+    2*want+16 candidate (i, j) draws, self-pairs dropped, pairs encoded as
+    lo*n + hi and merged through np.unique until enough are collected; the
+    smallest n_pairs codes are kept.  Asking for every pair enumerates them."""
+    n_all = n * (n - 1) // 2
+    want_total = min(DEFAULT_MAX_PAIRS if n_pairs is None else n_pairs, n_all)
+    if want_total == n_all:
+        return np.column_stack(np.triu_indices(n, k=1)).astype(np.int64)
+    rng = np.random.default_rng(seed)
+    un = np.uint64(n)
+    pool = np.empty(0, dtype=np.uint64)
+    while pool.size < want_total:
+        m = 2 * (want_total - pool.size) + 16
+        a, b = rng.integers(0, n, size=m), rng.integers(0, n, size=m)
+        keep = a != b
+        a, b = a[keep], b[keep]
+        fresh = np.minimum(a, b).astype(np.uint64) * un + np.maximum(a, b).astype(np.uint64)
+        pool = np.unique(np.concatenate([pool, fresh]))
+    pool = pool[:want_total]
+    return np.column_stack([pool // un, pool % un]).astype(np.int64)
+
+
+def _rows(x):
+    if isinstance(x, DeviceRows):
+        return x
+    if isinstance(x, EmbeddingMatrix):
+        x = x.values
+    x = getattr(x, "embedding", x)  # the reference's ExactEmbedding
+    a = np.asarray(x)
+    if a.dtype not in (np.float64, np.float32):
+        a = a.astype(np.float64)
+    if a.ndim != 2:
+        raise ValueError("expected a 2-d block of rows")
+    return np.ascontiguousarray(a)
+
+
+def _n_rows(x) -> int:
+    return x.n if isinstance(x, DeviceRows) else x.shape[0]
+
+
+def pair_correlations(rows, pairs, *, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """(cosine per pair, zero-norm flag per pair) -- _pair_correlations on the GPU."""
+    rows = _rows(rows)
+    pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1, 2))
+    out = np.zeros(len(pairs))
+    zero = np.zeros(len(pairs), dtype=np.uint8)
+    if isinstance(rows, DeviceRows):
+        ctx = _lib.context(rows.device)
+        rc = ctx.lib.csemb_pair_cosines(ctx.handle, C.c_void_p(rows.ptr), rows.dtype, 1, rows.n, rows.d, rows.ld,
+                                        _lib.ptr(pairs), len(pairs), _lib.ptr(out), _lib.ptr(zero))
+    else:
+        ctx = _lib.context(device)
+        code = _lib.F64 if rows.dtype == np.float64 else _lib.F32
+        n, d = rows.shape
+        rc = ctx.lib.csemb_pair_cosines(ctx.handle, _lib.ptr(rows), code, 0, n, d, d, _lib.ptr(pairs), len(pairs),
+                                        _lib.ptr(out), _lib.ptr(zero))
+    _lib.check(rc, "csemb_pair_cosines")
+    return out, zero.astype(bool)
+
+
+def normalized_correlation(X, i: int, j: int, *, device: int = 0) -> float:
+    """Cosine similarity of rows i and j; zero rows correlate as 0 (oracle.py:79-85)."""
+    return float(pair_correlations(X, np.array([[i, j]]), device=device)[0][0])
+
+
+@dataclass
+class CalibrationBin:
+    center: float
+    count: int
+    percentiles: dict[int, float]
+
+
+@dataclass
+class DistortionReport:
+    """Percentiles of correlation deviation, or per-bin calibration curves."""
+
+    mode: str
+    pair_sample_size: int
+    zero_row_pairs: int = 0
+    percentiles: dict[int, float] | None = None
+    bins: list[CalibrationBin] = field(default_factory=list)
+
+
+def _pct(values) -> dict[int, float]:
+    return dict(zip(PERCENTILE_LEVELS, (float(v) for v in np.percentile(values, PERCENTILE_LEVELS))))
+
+
+def _calibration_bins(exact_corr: np.ndarray, approx_corr: np.ndarray) -> list[CalibrationBin]:
+    """Bins of width 0.1 centred on -1.0 .. 1.0 by exact correlation (rounded
+    to the nearest centre, clipped); empty bins are omitted (oracle.py:166-181)."""
+    centres = np.round(np.arange(-1.0, 1.0 + CALIBRATION_BIN_WIDTH / 2, CALIBRATION_BIN_WIDTH), 10)
+    slot = np.clip(np.round((exact_corr + 1.0) / CALIBRATION_BIN_WIDTH).astype(int), 0, len(centres) - 1)
+    out = []
+    for b, centre in enumerate(centres):
+        members = approx_corr[slot == b]
+        if members.size:
+            out.append(CalibrationBin(center=float(centre), count=int(members.size), percentiles=_pct(members)))
+    return out
+
+
+def distortion_percentiles(exact, approx, n_pairs: int | None = None, seed: int = 0, mode: str = "deviation",
+                           *, device: int = 0) -> DistortionReport:
+    """Compare normalized correlations of two embeddings over sampled pairs
+    (oracle.py:139-186): ``deviation`` reports percentiles of approx - exact;
+    ``calibration`` bins pairs by exact correlation and reports percentiles
+    of the approximate correlation per bin.  Both correlation passes are
+    single device launches."""
+    X, Y = _rows(exact), _rows(approx)
+    if _n_rows(X) != _n_rows(Y):
+        raise ValueError("embeddings must have the same number of rows")
+    if mode not in ("deviation", "calibration"):
+        raise ValueError("mode must be 'deviation' or 'calibration'")
+    pairs = sample_pairs(_n_rows(X), n_pairs, seed)
+    cx, zx = pair_correlations(X, pairs, device=device)
+    cy, zy = pair_correlations(Y, pairs, device=device)
+    report = DistortionReport(mode=mode, pair_sample_size=len(pairs), zero_row_pairs=int(np.count_nonzero(zx | zy)))
+    if mode == "deviation":
+        report.percentiles = _pct(cy - cx)
+    else:
+        report.bins = _calibration_bins(cx, cy)
+    return report
+
+
+# -- report serialization (formats of oracle.py:227-275) ---------------------
+
+
+def report_to_dict(report: DistortionReport) -> dict:
+    doc = {"mode": report.mode, "pair_sample_size": report.pair_sample_size,
+           "zero_row_pairs": report.zero_row_pairs}
+    if report.percentiles is not None:
+        doc["percentiles"] = {str(level): v for level, v in report.percentiles.items()}
+    if report.bins:
+        doc["bins"] = [{"center": b.center, "count": b.count,
+                        "percentiles": {str(level): v for level, v in b.percentiles.items()}}
+                       for b in report.bins]
+    return doc
+
+
+def _write_csv(path, header, rows) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(header)
+        w.writerows(rows)
+
+
+def write_percentiles_csv(report: DistortionReport, path) -> None:
+    if report.percentiles is None:
+        raise ValueError("report has no deviation percentiles")
+    _write_csv(path, ["percentile", "value"], ([p, repr(report.percentiles[p])] for p in PERCENTILE_LEVELS))
+
+
+def write_calibration_csv(report: DistortionReport, path) -> None:
+    if not report.bins:
+        raise ValueError("report has no calibration bins")
+    _write_csv(path, ["bin_center"] + [f"p{p}" for p in PERCENTILE_LEVELS],
+               ([b.center] + [repr(b.percentiles[p]) for p in PERCENTILE_LEVELS] for b in report.bins))
+
+
+def write_report_json(report: DistortionReport, path) -> None:
+    with open(path, "w") as fh:
+        json.dump(report_to_dict(report), fh, indent=2, sort_keys=True)
+        fh.write("\n")

@@ -591,6 +591,12 @@ def install(csemb_module):
     def proj(n, d, seed):
         return sample_projection(n, d, seed)
 
+    from . import cluster as dev_cluster
+    from . import distortion as dev_distortion
+
+    def pair_corr(rows, pairs):
+        return dev_distortion.pair_correlations(rows, pairs)
+
     base = csemb_module.__name__
     for sub in ("engine", "oracle", "cli", "cluster"):
         try:
@@ -600,6 +606,11 @@ def install(csemb_module):
         patch(mod, "_apply_expansion", seam)
         patch(mod, "estimate_spectral_norm", norm)
         patch(mod, "sample_projection", proj)
+        if sub == "cluster":  # downstream consumers (cluster.py:59-128)
+            patch(mod, "kmeans", dev_cluster.kmeans)
+            patch(mod, "modularity", dev_cluster.modularity)
+        if sub == "oracle":  # sampled-pair correlations (oracle.py:88-96)
+            patch(mod, "_pair_correlations", pair_corr)
     patch(csemb_module, "estimate_spectral_norm", norm)
     patch(csemb_module, "sample_projection", proj)
 

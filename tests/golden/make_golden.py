@@ -357,7 +357,72 @@ def gen_cli():
     _save("cli", meta, **arrays)
 
 
+def _dup_points():
+    """30 rows on 5 distinct points: with K=8 the ++ seeding runs out of
+    positive distance (total <= 0 branch) and Lloyd meets empty clusters."""
+    rng = np.random.default_rng(17)
+    base = rng.standard_normal((5, 6))
+    return base[rng.integers(0, 5, size=30)]
+
+
+def _blobs(n, d, k, seed):
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((k, d)) * 4.0
+    return centers[rng.integers(0, k, size=n)] + rng.standard_normal((n, d))
+
+
+def gen_downstream():
+    """Downstream consumers: cluster.kmeans, cluster.modularity,
+    cluster.cluster_experiment, oracle._pair_correlations and
+    oracle.distortion_percentiles on the config-1 embedding, plus k-means on
+    Gaussian blobs (K=70: two centroid tiles) and on duplicated points."""
+    from csemb import cluster as ccl
+    from csemb import oracle as cor
+
+    edges, labels = sbm(2000, 4, 0.05, 0.005, np.random.default_rng(0))
+    S = cs.normalized_adjacency(edges, 2000)
+    f = cs.indicator_above(0.9)
+    emb = cs.fast_embed_eig(S, f, 60, cs.sample_projection(2000, 40, 0))
+    E = emb.values
+    arrays, meta = {}, {"kmeans": {}, "modularity": {}}
+    inputs = {"config1": E, "blobs": _blobs(3000, 20, 70, 5), "dup": _dup_points()}
+    arrays["blobs_X"] = inputs["blobs"]
+    arrays["dup_X"] = inputs["dup"]
+    cases = [("config1", 4, 0x6B6D6531), ("config1", 4, 0x6B6D6532), ("config1", 9, 7),
+             ("blobs", 70, 11), ("blobs", 3, 2), ("dup", 8, 4), ("dup", 1, 0)]
+    for name, K, seed in cases:
+        km = ccl.kmeans(inputs[name], K, seed=seed)
+        key = f"{name}_K{K}_s{seed}"
+        arrays[f"km_{key}_labels"] = km.labels.astype(np.int16)
+        arrays[f"km_{key}_history"] = np.array(km.inertia_history)
+        meta["kmeans"][key] = {"input": name, "K": K, "seed": seed, "n_iters": km.n_iters,
+                               "inertia": km.inertia}
+        if name == "config1":
+            q = ccl.modularity(edges, km)
+            meta["modularity"][key] = {"Q": q.Q, "m_edges": q.m_edges}
+    q = ccl.modularity(edges, labels)
+    meta["modularity"]["truth"] = {"Q": q.Q, "m_edges": q.m_edges}
+    ex = ccl.cluster_experiment(edges, 2000, f, cs.EmbedConfig(L=60, d=40, seed=0), K=4, runs=5)
+    meta["experiment"] = {"call": "cluster_experiment(edges, 2000, indicator_above(0.9), EmbedConfig(L=60,d=40,seed=0), K=4, runs=5)",
+                          "median_modularity": ex.median_modularity, "run_scores": list(ex.run_scores)}
+    arrays["experiment_median_labels"] = ex.median_labels.astype(np.int16)
+    pairs = cs.sample_pairs(2000, 10_000, 0)
+    cos, zero = cor._pair_correlations(E, pairs)
+    arrays["pair_cos"] = cos
+    exact = cor.exact_embedding(S, f)
+    arrays["exact_embedding"] = exact.embedding
+    for mode in ("deviation", "calibration"):
+        rep = cor.distortion_percentiles(exact, emb, n_pairs=20_000, seed=3, mode=mode)
+        meta[f"distortion_{mode}"] = cor.report_to_dict(rep)
+    meta["distortion_call"] = "distortion_percentiles(exact_embedding(S, f), emb, n_pairs=20000, seed=3, mode)"
+    _save("downstream", meta, **arrays)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
     gen_omega()
     gen_config1()
     gen_small_cases()
@@ -365,3 +430,4 @@ if __name__ == "__main__":
     gen_norm()
     gen_builders()
     gen_cli()
+    gen_downstream()

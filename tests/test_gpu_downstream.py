@@ -1,0 +1,227 @@
+"""Downstream consumers on the device vs the reference's
+fixtures and the oracle (B200 only).
+
+Bars: labels, iteration counts and modularity identical to the reference;
+inertia histories within 1e-10 relative (the reference's X @ C.T comes from
+BLAS in unspecified order; ours follows numpy's pairwise order); centroids
+bit-identical to np.add.at means of the same labels; pair cosines within
+1e-12; distortion percentiles within 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1509_08360_b200 as pb
+from conftest import load_golden, sparse_from
+from paper_1509_08360_b200 import cluster as pcl
+from paper_1509_08360_b200 import distortion as D
+
+pytestmark = pytest.mark.gpu
+
+HIST_REL = 1e-10
+COS_ABS = 1e-12
+
+
+@pytest.fixture(autouse=True)
+def _lib_ready(gpu_lib):
+    yield
+
+
+@pytest.fixture(scope="module")
+def ds():
+    return load_golden("downstream")
+
+
+@pytest.fixture(scope="module")
+def rows(ds, config1):
+    z, _ = ds
+    c1, _ = config1
+    return {"config1": c1["E"], "blobs": z["blobs_X"], "dup": z["dup_X"]}
+
+
+def _means(X, labels, K):
+    acc = np.zeros((K, X.shape[1]))
+    np.add.at(acc, labels, X)
+    return acc / np.bincount(labels, minlength=K)[:, None]
+
+
+def _close_hist(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape
+    assert np.all(np.abs(got - want) <= HIST_REL * np.maximum(np.abs(want), 1e-300) + 1e-300), (got, want)
+
+
+class TestKMeans:
+    def test_reference_fixtures(self, ds, rows):
+        z, meta = ds
+        for key, m in meta["kmeans"].items():
+            a = pcl.kmeans(rows[m["input"]], m["K"], seed=m["seed"])
+            assert np.array_equal(a.labels, z[f"km_{key}_labels"]), key
+            assert a.n_iters == m["n_iters"], key
+            _close_hist(a.inertia_history, z[f"km_{key}_history"])
+
+    def test_duplicate_points_exact_zero_distances(self, ds, rows):
+        """Identical rows have distance exactly 0 (pairwise-order dots): the
+        zero-total seeding branch and the reseed argmax follow the reference."""
+        z, meta = ds
+        a = pcl.kmeans(rows["dup"], 8, seed=4)
+        assert a.inertia == 0.0 and set(a.inertia_history) == {0.0}
+        assert np.array_equal(a.labels, z["km_dup_K8_s4_labels"])
+
+    def test_centroids_bit_identical_to_add_at_means(self, rows):
+        X = rows["blobs"]
+        km = pcl.DeviceKMeans(X, 3)
+        try:
+            a = pcl.kmeans(X, 3, seed=2, handle=km)
+            assert a.n_iters < 100  # converged: centroids are the means of the final labels
+            assert np.array_equal(km.centroids(), _means(X, a.labels, 3))
+        finally:
+            km.close()
+
+    @pytest.mark.parametrize("n,d,K,seed", [
+        (3000, 80, 200, 1),   # centroids staged per 32-wide tile (no CFULL)
+        (2500, 150, 6, 2),    # d > 128: several pairwise leaves (k_km_assign_wide)
+        (1500, 3, 5, 3),      # d < 8: sequential pairwise leaf
+        (4000, 129, 9, 4),    # first d with a split
+        (777, 17, 64, 5),     # ragged tiles
+    ])
+    def test_against_oracle(self, n, d, K, seed):
+        rng = np.random.default_rng(seed)
+        centers = rng.standard_normal((K, d)) * 3.0
+        X = centers[rng.integers(0, K, size=n)] + rng.standard_normal((n, d))
+        a = pcl.kmeans(X, K, seed=seed)
+        labels, hist = O.kmeans(X, K, seed=seed)
+        assert np.array_equal(a.labels, labels)
+        _close_hist(a.inertia_history, hist)
+
+    def test_device_rows_and_f32(self, config1):
+        """K-means straight from a plan's device-resident E (fp64 and fp32)."""
+        c1, _ = config1
+        S = sparse_from(c1)
+        for dtype in ("float64", "float32"):
+            dm = pb.DeviceMatrix(S, dtype)
+            plan = dm.plan(40)
+            plan.run(c1["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+            E = plan.download()
+            a = pcl.kmeans(pcl.plan_rows(plan), 4, seed=0x6B6D6531)
+            b = pcl.kmeans(E, 4, seed=0x6B6D6531)
+            assert np.array_equal(a.labels, b.labels) and a.inertia_history == b.inertia_history
+            dm.close()
+
+    def test_deterministic_and_errors(self, rows):
+        X = rows["config1"]
+        a, b = pcl.kmeans(X, 9, seed=7), pcl.kmeans(X, 9, seed=7)
+        assert np.array_equal(a.labels, b.labels) and a.inertia_history == b.inertia_history
+        for K in (0, len(X) + 1):
+            with pytest.raises(ValueError):
+                pcl.kmeans(X, K)
+
+    def test_single_row_and_k_equals_n(self):
+        X = np.arange(12, dtype=np.float64).reshape(4, 3)
+        for K in (1, 4):
+            a = pcl.kmeans(X, K, seed=1)
+            labels, hist = O.kmeans(X, K, seed=1)
+            assert np.array_equal(a.labels, labels)
+            _close_hist(a.inertia_history, hist)
+        a = pcl.kmeans(X[:1], 1)
+        assert a.labels.tolist() == [0] and a.inertia == 0.0
+
+
+class TestModularity:
+    def test_reference_fixtures(self, ds, config1):
+        z, meta = ds
+        c1, _ = config1
+        q = pcl.modularity(c1["edges"], c1["labels"])
+        assert (q.Q, q.m_edges) == (meta["modularity"]["truth"]["Q"], meta["modularity"]["truth"]["m_edges"])
+        for key, want in meta["modularity"].items():
+            if key != "truth":
+                q = pcl.modularity(c1["edges"], z[f"km_{key}_labels"])
+                assert q.Q == want["Q"], key
+
+    def test_duplicates_loops_and_errors(self):
+        edges = np.array([[0, 1], [1, 0], [1, 2], [2, 2], [2, 3], [3, 0], [0, 1]])
+        lab = np.array([0, 0, 1, 1])
+        q = pcl.modularity(edges, lab)
+        want, m = O.modularity(edges, lab)
+        assert q.Q == want and q.m_edges == m == 4
+        with pytest.raises(ValueError):
+            pcl.modularity(np.array([[1, 1]]), lab)
+        with pytest.raises(ValueError):
+            pcl.modularity(edges, lab[:3])
+
+    def test_large_random_graph(self):
+        n = 200_000
+        edges = np.random.default_rng(5).integers(0, n, size=(1_000_000, 2))
+        lab = np.random.default_rng(6).integers(0, 37, size=n)
+        q = pcl.modularity(edges, lab)
+        want, m = O.modularity(edges, lab)
+        assert q.Q == want and q.m_edges == m
+
+
+class TestPairsAndDistortion:
+    def test_pair_cosines_vs_reference(self, ds, config1):
+        z, _ = ds
+        c1, _ = config1
+        cos, zero = D.pair_correlations(c1["E"], c1["pairs"].astype(np.int64))
+        assert np.max(np.abs(cos - z["pair_cos"])) <= COS_ABS and not zero.any()
+
+    def test_zero_rows_and_f32(self):
+        rng = np.random.default_rng(1)
+        E = rng.standard_normal((300, 37))
+        E[[3, 77]] = 0.0
+        pairs = np.array([[3, 5], [5, 77], [3, 77], [1, 2], [0, 299]])
+        cos, zero = D.pair_correlations(E, pairs)
+        assert zero.tolist() == [True, True, True, False, False]
+        assert np.all(cos[:3] == 0.0)
+        assert np.max(np.abs(cos - O.pair_cosines(E, pairs))) <= COS_ABS
+        c32, _ = D.pair_correlations(E.astype(np.float32), pairs)
+        assert np.max(np.abs(c32 - O.pair_cosines(E.astype(np.float32).astype(np.float64), pairs))) <= COS_ABS
+        wide = rng.standard_normal((50, 300))
+        pw = D.sample_pairs(50, 200, 0)
+        assert np.max(np.abs(D.pair_correlations(wide, pw)[0] - O.pair_cosines(wide, pw))) <= COS_ABS
+        with pytest.raises(ValueError):
+            D.pair_correlations(E, np.array([[0, 300]]))
+
+    def test_distortion_report_vs_reference(self, ds, config1):
+        z, meta = ds
+        c1, _ = config1
+        for mode in ("deviation", "calibration"):
+            rep = D.report_to_dict(D.distortion_percentiles(z["exact_embedding"], c1["E"], n_pairs=20_000, seed=3,
+                                                            mode=mode))
+            want = meta[f"distortion_{mode}"]
+            assert rep["pair_sample_size"] == want["pair_sample_size"]
+            assert rep["zero_row_pairs"] == want["zero_row_pairs"]
+            if mode == "deviation":
+                for k, v in want["percentiles"].items():
+                    assert abs(rep["percentiles"][k] - v) <= 1e-10
+            else:
+                assert [(b["center"], b["count"]) for b in rep["bins"]] == [(b["center"], b["count"])
+                                                                            for b in want["bins"]]
+                for gb, wb in zip(rep["bins"], want["bins"]):
+                    for k, v in wb["percentiles"].items():
+                        assert abs(gb["percentiles"][k] - v) <= 1e-10
+
+    def test_device_resident_embedding(self, config1):
+        """North-star cosine check without downloading E: fp32 device rows vs
+        the fp64 reference on the config-1 pairs (<= 1e-4)."""
+        c1, _ = config1
+        dm = pb.DeviceMatrix(sparse_from(c1), "float32")
+        plan = dm.plan(40)
+        plan.run(c1["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+        cos, _ = D.pair_correlations(pcl.plan_rows(plan), c1["pairs"].astype(np.int64))
+        assert np.max(np.abs(cos - O.pair_cosines(c1["E"], c1["pairs"]))) <= 1e-4
+        dm.close()
+
+
+def test_cluster_experiment_matches_reference(ds):
+    z, meta = ds
+    ex_meta = meta["experiment"]
+    c1, _ = load_golden("config1")
+    ex = pcl.cluster_experiment(c1["edges"].astype(np.int64), 2000, pb.indicator_above(0.9),
+                                pb.EmbedConfig(L=60, d=40, seed=0), K=4, runs=5)
+    assert list(ex.run_scores) == ex_meta["run_scores"]
+    assert ex.median_modularity == ex_meta["median_modularity"]
+    assert np.array_equal(ex.median_labels, z["experiment_median_labels"])
+    with pytest.raises(ValueError):
+        pcl.cluster_experiment(c1["edges"], 2000, pb.indicator_above(0.9), pb.EmbedConfig(L=60, d=40), K=4, runs=0)

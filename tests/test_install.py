@@ -63,3 +63,21 @@ def test_install_patches_every_module(csemb):
         restore()
     for m in ("engine", "oracle"):
         assert getattr(importlib.import_module(f"csemb.{m}"), "_apply_expansion") is before[m]
+
+
+def test_install_patches_downstream_consumers(csemb):
+    import importlib
+
+    cl = importlib.import_module("csemb.cluster")
+    orc = importlib.import_module("csemb.oracle")
+    before = (cl.kmeans, cl.modularity, orc._pair_correlations)
+    restore = pb.install(csemb)
+    try:
+        assert cl.kmeans is pb.kmeans and cl.modularity is pb.modularity
+        assert orc._pair_correlations is not before[2]
+        if pb._lib.device_count() == 0:
+            with pytest.raises(pb.CudaUnavailableError):
+                cl.kmeans(np.eye(4), 2)
+    finally:
+        restore()
+    assert (cl.kmeans, cl.modularity, orc._pair_correlations) == before
