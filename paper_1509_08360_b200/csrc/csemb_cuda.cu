@@ -414,9 +414,26 @@ extern "C" int csemb_ctx_destroy(csemb_ctx *c) {
     if (!c) return CSEMB_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    cudaFree(c->scratch);
     cudaStreamDestroy(c->stream);
     delete c;
     return CSEMB_OK;
+}
+
+cudaError_t ctx_scratch(csemb_ctx *c, size_t bytes, void **out) {
+    if (bytes > c->scratch_bytes) {
+        cudaError_t e = cudaStreamSynchronize(c->stream);  // the old buffer may still be in use
+        if (e != cudaSuccess) return e;
+        cudaFree(c->scratch);
+        c->scratch = nullptr;
+        c->scratch_bytes = 0;
+        const size_t grow = std::max(bytes, (size_t)1 << 20);
+        e = cudaMalloc(&c->scratch, grow);
+        if (e != cudaSuccess) return e;
+        c->scratch_bytes = grow;
+    }
+    *out = c->scratch;
+    return cudaSuccess;
 }
 
 extern "C" void *csemb_ctx_stream(csemb_ctx *c) { return c ? (void *)c->stream : nullptr; }

@@ -45,7 +45,7 @@ struct csemb_kmeans {
     int *lab_new = nullptr;     // labels of the last assignment
     unsigned long long *counts = nullptr;  // K (+1: changed counter at counts[K])
     double *part = nullptr;     // n_chunks partial sums
-    int64_t *part_i = nullptr;  // n_chunks argmax indices
+    int64_t *part_i = nullptr;  // n_chunks argmax indices; K label totals in commit
     double *scal = nullptr;     // [0] closest total, [1] inertia
     int64_t *pick = nullptr;    // [0] picked / reseeded row
     int64_t *seg_off = nullptr, *order = nullptr, *start = nullptr;
@@ -79,14 +79,13 @@ extern "C" int csemb_pair_cosines(csemb_ctx *c, const void *E, int dtype, int on
     CK(cudaSetDevice(c->device));
     if (n_pairs == 0) return CSEMB_OK;
     const size_t es = dsize(dtype);
-    int64_t *dp = nullptr;
-    double *dout = nullptr;
-    uint8_t *dz = nullptr;
+    void *scr = nullptr;
     void *dE = nullptr;
     cudaStream_t s = c->stream;
-    cudaError_t e = cudaMalloc(&dp, 16 * n_pairs);
-    if (e == cudaSuccess) e = cudaMalloc(&dout, 8 * n_pairs);
-    if (e == cudaSuccess) e = cudaMalloc(&dz, n_pairs);
+    cudaError_t e = ctx_scratch(c, 25 * (size_t)n_pairs + 64, &scr);  // pairs, cosines, flags
+    int64_t *dp = (int64_t *)scr;
+    double *dout = (double *)(dp + 2 * n_pairs);
+    uint8_t *dz = (uint8_t *)(dout + n_pairs);
     if (e == cudaSuccess && !on_device) {  // host block: one upload, row stride d
         e = cudaMalloc(&dE, es * n * d);
         if (e == cudaSuccess) e = cudaMemcpy2DAsync(dE, es * d, E, es * ld, es * d, n, cudaMemcpyHostToDevice, s);
@@ -105,9 +104,6 @@ extern "C" int csemb_pair_cosines(csemb_ctx *c, const void *E, int dtype, int on
     if (e == cudaSuccess) e = cudaMemcpyAsync(cos_out, dout, 8 * n_pairs, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && zero_out) e = cudaMemcpyAsync(zero_out, dz, n_pairs, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(dp);
-    cudaFree(dout);
-    cudaFree(dz);
     cudaFree(dE);
     CK(e);
     return CSEMB_OK;
@@ -159,7 +155,7 @@ extern "C" int csemb_kmeans_create(csemb_ctx *c, const void *X, int dtype, int o
     A((void **)&k->lab_new, 4 * n);
     A((void **)&k->counts, 8 * ((size_t)K + 1));
     A((void **)&k->part, 8 * m);
-    A((void **)&k->part_i, 8 * m);
+    A((void **)&k->part_i, 8 * std::max<int64_t>(m, K));  // argmax indices / label totals
     A((void **)&k->scal, 16);
     A((void **)&k->pick, 8);
     A((void **)&k->seg_off, 8 * (size_t)k->nseg * K);
@@ -241,7 +237,7 @@ extern "C" int csemb_kmeans_pick(csemb_kmeans *k, double u, int64_t *row) {
     cudaStream_t s = c->stream;
     const int64_t m = n_chunks(k->n);
     k_chunk_sums<<<(unsigned)m, RED_THREADS, 0, s>>>(k->closest, k->n, RED_CHUNK, k->scal, k->part);
-    k_km_pick<<<1, 32, 0, s>>>(k->closest, k->n, RED_CHUNK, k->part, m, k->scal, u, k->pick);
+    k_km_pick<<<1, 1024, 0, s>>>(k->closest, k->n, RED_CHUNK, k->part, m, k->scal, u, k->pick);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(row, k->pick, 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -259,17 +255,16 @@ extern "C" int csemb_kmeans_assign(csemb_kmeans *k, double *inertia, int64_t *ch
     CK(cudaMemsetAsync(k->counts, 0, 8 * ((size_t)K + 1), s));
     const int64_t tiles = (k->n + KA_TM - 1) / KA_TM;
     if (k->d <= KA_MAXD) {
-        const int dp = k->d | 1;
+        const KaGeom geo(k->d);
         const int Kp = (K + KA_TK - 1) / KA_TK * KA_TK;
-        const size_t base = 8 * (size_t)KA_TM * dp + 4 * (size_t)K;
-        const size_t full = base + 8 * (size_t)Kp * dp, tiled = base + 8 * (size_t)KA_TK * dp;
-        const bool cfull = full <= 110 * 1024;  // two CTAs per SM
+        const size_t base = 16 * (size_t)KA_TM * geo.rs + 12 * 4 * (size_t)KA_TM + 4 * (size_t)K;
+        const size_t full = base + 8 * (size_t)Kp * geo.rs, tiled = base + 8 * (size_t)KA_TK * geo.rs;
+        const bool cfull = full <= 220 * 1024;  // one 512-thread CTA per SM
         const size_t smem = cfull ? full : tiled;
         if (smem > 220 * 1024) return fail(CSEMB_ERR_UNSUPPORTED, "K=%d exceeds the shared-memory histogram", K);
         const void *fn = cfull ? (const void *)k_km_assign<true> : (const void *)k_km_assign<false>;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        const int per_sm = smem <= 110 * 1024 ? 2 : 1;
-        const int g = (int)std::min<int64_t>(tiles, (int64_t)c->sm_count * per_sm);
+        const int g = (int)std::min<int64_t>(tiles, (int64_t)c->sm_count);
         if (cfull)
             k_km_assign<true><<<g, KA_THREADS, smem, s>>>(k->X, k->n, k->d, k->ld, k->xx, k->C, K, k->ldc, k->cc,
                                                           k->lab, k->lab_new, k->mind, k->counts, k->counts + K);
@@ -327,12 +322,14 @@ extern "C" int csemb_kmeans_commit(csemb_kmeans *k, int update_centroids) {
         if (hsmem > 48 * 1024)
             CK(cudaFuncSetAttribute(k_km_seg_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
         k_km_seg_hist<<<(unsigned)k->nseg, 256, hsmem, s>>>(k->lab, k->n, K, k->seg, k->seg_off);
-        k_km_seg_scan<<<1, 1024, 0, s>>>(k->seg_off, k->nseg, K, k->start);
+        k_km_seg_scan<<<(unsigned)((K + 7) / 8), 256, 0, s>>>(k->seg_off, k->nseg, K, k->part_i);
+        k_km_start_scan<<<1, 1024, 0, s>>>(k->part_i, K, k->start);
         k_km_seg_scatter<<<(unsigned)((k->nseg + 3) / 4), 128, 0, s>>>(k->lab, k->n, K, k->seg, k->seg_off,
-                                                                        k->order);
+                                                                        k->start, k->order);
         const int64_t warps = (int64_t)K * ((k->d + 31) / 32);
-        k_km_sums<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(k->X, k->d, k->ld, k->order, k->start, K, k->C,
-                                                              k->ldc);
+        const int ring = KS_D * 32 * 32 * 8;
+        CK(cudaFuncSetAttribute(k_km_sums, cudaFuncAttributeMaxDynamicSharedMemorySize, ring));
+        k_km_sums<<<(unsigned)warps, 32, ring, s>>>(k->X, k->d, k->ld, k->order, k->start, K, k->C, k->ldc);
         CK(cudaGetLastError());
     }
     return CSEMB_OK;

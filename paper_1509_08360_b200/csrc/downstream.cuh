@@ -29,6 +29,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <climits>
+
 namespace csemb {
 
 // ---------------------------------------------------------------------------
@@ -88,7 +90,7 @@ __device__ __forceinline__ double sumsq_group8(const T *a, int n, int j) {
 }
 
 // np.maximum(d2, 0.0) / np.minimum(a, b) semantics: (a >= b || isnan(a)) ? a : b
-__device__ __forceinline__ double np_max0(double v) { return (v >= 0.0 || isnan(v)) ? v : 0.0; }
+__device__ __forceinline__ double np_max0(double v) { return v < 0.0 ? 0.0 : v; }  // keeps NaN and -0.0
 __device__ __forceinline__ double np_min(double a, double b) { return (a <= b || isnan(a)) ? a : b; }
 
 // ---------------------------------------------------------------------------
@@ -195,43 +197,103 @@ __global__ void k_sum_final(const double *__restrict__ part, int64_t m, double *
     if (threadIdx.x == 0) *out = s;
 }
 
+// block-wide exclusive scan of one value per thread; *total = the block sum
+__device__ __forceinline__ double block_excl_scan(double v, double *sh, double &total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) sh[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        double x = lane < nw ? sh[lane] : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
+        }
+        sh[lane] = x;
+    }
+    __syncthreads();
+    const double base = w ? sh[w - 1] : 0.0;
+    total = sh[nw - 1];
+    __syncthreads();
+    return base + inc - v;
+}
+
 // ++ pick (cluster.py:53): rng.choice(n, p=closest/total) == first i with
 // cumsum(p)[i] / cumsum(p)[-1] > u (verified against numpy's Generator.choice).
-// Chunk sums locate the chunk; the element scan is sequential from there.
-__global__ void k_km_pick(const double *__restrict__ closest, int64_t n, int64_t chunk,
-                          const double *__restrict__ part, int64_t m, const double *__restrict__ total, double u,
-                          int64_t *__restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double T = 0.0;
-    for (int64_t c = 0; c < m; ++c) T += part[c];
+// One block: a block scan over the chunk sums finds the chunk, a block scan
+// over that chunk's p_i = closest_i / total finds the element (fixed order,
+// deterministic; the prefix rounding is not numpy's sequential cumsum).
+__global__ void __launch_bounds__(1024) k_km_pick(const double *__restrict__ closest, int64_t n, int64_t chunk,
+                                                  const double *__restrict__ part, int64_t m,
+                                                  const double *__restrict__ total, double u,
+                                                  int64_t *__restrict__ out) {
+    __shared__ double sh[32];
+    __shared__ long long s_c, s_pick;
+    __shared__ double s_base;
+    const int t = threadIdx.x, nt = blockDim.x;
     const double tot = *total;
-    double s = 0.0;
-    int64_t c = 0;
-    for (; c < m; ++c) {
-        if ((s + part[c]) / T > u) break;
-        s += part[c];
-    }
-    if (c == m) c = m - 1, s -= part[m - 1];
-    int64_t pick = -1, last_pos = -1;
-    for (int64_t i = c * chunk; i < n; ++i) {
-        const double p = closest[i] / tot;
-        if (p > 0.0) last_pos = i;
-        s += p;
-        if (s / T > u && p > 0.0) {
-            pick = i;
+    // chunk level
+    const int64_t per = (m + nt - 1) / nt, lo = min(m, (int64_t)t * per), hi = min(m, lo + per);
+    double loc = 0.0;
+    for (int64_t c = lo; c < hi; ++c) loc += part[c];
+    double T;
+    const double ex = block_excl_scan(loc, sh, T);
+    if (t == 0) s_c = m, s_pick = LLONG_MAX;
+    __syncthreads();
+    double run = ex;
+    for (int64_t c = lo; c < hi; ++c) {
+        if ((run + part[c]) / T > u) {
+            atomicMin(&s_c, (long long)c);
             break;
         }
+        run += part[c];
     }
-    if (pick < 0) {  // rounding left u above the scanned total: last positive entry
-        if (last_pos < 0)
-            for (int64_t i = c * chunk - 1; i >= 0; --i)
+    __syncthreads();
+    int64_t c0 = s_c < m ? s_c : m - 1;
+    if (c0 >= lo && c0 < hi) {  // the owner of chunk c0 knows the prefix before it
+        double b = ex;
+        for (int64_t c = lo; c < c0; ++c) b += part[c];
+        s_base = b;
+    }
+    __syncthreads();
+    double base = s_base;
+    // element level, from chunk c0 on (later chunks only if rounding moved the crossing)
+    for (int64_t c = c0; c < m; ++c) {
+        const int64_t elo = c * chunk, ehi = min(n, elo + chunk);
+        const int64_t eper = (ehi - elo + nt - 1) / nt;
+        const int64_t a = min(ehi, elo + (int64_t)t * eper), z = min(ehi, a + eper);
+        double ls = 0.0;
+        for (int64_t i = a; i < z; ++i) ls += closest[i] / tot;
+        double ct;
+        double r = base + block_excl_scan(ls, sh, ct);
+        for (int64_t i = a; i < z; ++i) {
+            const double p = closest[i] / tot;
+            r += p;
+            if (p > 0.0 && r / T > u) {
+                atomicMin(&s_pick, (long long)i);
+                break;
+            }
+        }
+        __syncthreads();
+        if (s_pick != LLONG_MAX) break;
+        base += ct;
+    }
+    if (t == 0) {
+        int64_t pick = s_pick;
+        if (pick == LLONG_MAX) {  // u above the rounded total: the last positive entry
+            pick = 0;
+            for (int64_t i = n - 1; i >= 0; --i)
                 if (closest[i] > 0.0) {
-                    last_pos = i;
+                    pick = i;
                     break;
                 }
-        pick = last_pos < 0 ? 0 : last_pos;
+        }
+        *out = pick;
     }
-    *out = pick;
 }
 
 // first index of the maximum (np.argmax) -- two stages: per block, then final
@@ -285,132 +347,219 @@ __global__ void k_km_reseed(const double *__restrict__ pv, const int64_t *__rest
 // K8: Lloyd assignment (cluster.py:74-77): labels = argmin_k d2, mindist,
 // with d2 = max((xx + cc) - 2 x.c, 0) (cluster.py:34-40).
 //
-// k_km_assign (d <= 128, one pairwise leaf): CTA tile of 32 rows x 32
-// centroids; the rows of the tile and the centroids (all of them when they
-// fit, CFULL, else one 32-centroid tile at a time) are staged in shared memory
-// with an odd row stride.  8-lane group g of the CTA owns a 4-row x 8-centroid
-// micro-tile; lane j of the group is residue class j of numpy's 8-accumulator
-// sum, so after the body three xor-shuffles (tree8) and the in-order d % 8
-// tail give x.c with exactly np.sum(x*c)'s rounding.  The 4 groups of a warp
-// share the row quad and cover the tile's 32 centroids; the running
-// lexicographic (d2, k) minimum is np.argmin's first-minimum rule.  Epilogue:
-// label / min-distance store, #changed vs the previous labels, per-cluster
-// counts (shared histogram, one atomic per cluster per block).
+// k_km_assign (d <= 128, one pairwise leaf).  One 512-thread CTA per SM; a
+// CTA step covers 64 rows x 16 centroids.  Warp w owns 16 rows (4 row quads,
+// one per 8-lane group) x one centroid quartet; lane j of a group is residue
+// class j of numpy's 8-accumulator pairwise sum, so after the body three
+// xor-shuffles (tree8) and the in-order d % 8 tail give x.c with exactly
+// np.sum(x*c)'s rounding.  Shared memory holds rows and centroids
+// residue-major -- element c at [c % 8][c / 8], residue length padded to
+// 2 mod 4 (conflict-free 16-byte reads, two body steps per load) -- with the
+// row tiles double-buffered through cp.async and the centroids staged once
+// per CTA when they fit (CFULL).  Quartets past K are skipped (warp-uniform).
+// Each thread keeps its rows' running minimum over its quartets in ascending k
+// (strict <: np.argmin's first minimum); the four quartet warps of a row merge
+// once per row tile through shared memory.  The 8 residue lanes reduce by a
+// transpose-reduce in numpy's tree order, leaving each lane 2 finished dot
+// products, so the tail, the d2 epilogue and the argmin run once per (row,
+// centroid) pair rather than once per lane.  Epilogue: label / min-distance
+// store, #changed vs the previous labels, per-cluster counts.
 // ---------------------------------------------------------------------------
-constexpr int KA_TM = 32, KA_TK = 32, KA_THREADS = 256, KA_MAXD = 128;
+constexpr int KA_TM = 64, KA_TK = 16, KA_THREADS = 512, KA_MAXD = 128;
+
+// 8-byte async copy global -> shared (src_bytes 0 zero-fills), commit / wait
+__device__ __forceinline__ void ca8(double *dst, const double *src, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void ca_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void ca_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void lexmin(double &bd, int &bk, double od, int ok) {
     if (od < bd || (od == bd && ok < bk)) bd = od, bk = ok;
 }
 
+// residue-major geometry of one row: body elements c < body at [c % 8][c / 8]
+// (residue length tp), tail elements at 8 * tp + (c - body); row stride rs
+struct KaGeom {
+    int body, tp, rs;
+    __host__ __device__ KaGeom(int d) {
+        body = d < 8 ? 0 : d - d % 8;
+        const int t = body / 8;
+        tp = t == 0 ? 0 : (t % 4 == 2 ? t : t + ((2 - t % 4) + 4) % 4);
+        rs = 8 * tp + 8;
+    }
+    __device__ __forceinline__ int pos(int c) const { return c < body ? (c & 7) * tp + (c >> 3) : 8 * tp + (c - body); }
+};
+
 template <bool CFULL>
-__global__ void __launch_bounds__(KA_THREADS) k_km_assign(
+__global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
     const double *__restrict__ X, int64_t n, int d, int64_t ld, const double *__restrict__ xx,
     const double *__restrict__ C, int K, int64_t ldc, const double *__restrict__ cc,
     const int *__restrict__ lab_old, int *__restrict__ lab_new, double *__restrict__ mind,
     unsigned long long *__restrict__ counts, unsigned long long *__restrict__ changed) {
     extern __shared__ __align__(16) double sm[];
-    const int dp = d | 1;                      // odd stride: 4 centroid rows hit 2 bank halves
+    const KaGeom G(d);
+    const int T = G.body / 8;
     const int Kp = (K + KA_TK - 1) / KA_TK * KA_TK;
-    double *Xs = sm;                           // [KA_TM][dp]
-    double *Cs = Xs + KA_TM * dp;              // [CFULL ? Kp : KA_TK][dp]
-    unsigned *s_cnt = reinterpret_cast<unsigned *>(Cs + (CFULL ? Kp : KA_TK) * dp);
-    const int tid = threadIdx.x, j = tid & 7, g = tid >> 3;
-    const int rq = (g >> 2) * 4;               // this group's 4 rows within the tile
-    const int co = (g & 3) * 8;                // this group's 8 centroids within the tile
-    const int body = d < 8 ? 0 : d - (d % 8);
+    double *Xb = sm;                                 // [2][KA_TM][rs] row tiles
+    double *Cs = Xb + 2 * KA_TM * G.rs;              // [CFULL ? Kp : KA_TK][rs]
+    double *cand_d = Cs + (CFULL ? Kp : KA_TK) * G.rs;  // [4 quartets][KA_TM]
+    int *cand_k = reinterpret_cast<int *>(cand_d + 4 * KA_TM);
+    unsigned *s_cnt = reinterpret_cast<unsigned *>(cand_k + 4 * KA_TM);
+    const int tid = threadIdx.x, j = tid & 7, w = tid >> 5;
+    const int oct = w & 3;                           // centroid quartet within a 16-tile
+    const int rq = (w >> 2) * 16 + ((tid >> 3) & 3) * 4;  // this group's 4 rows within the tile
+    const int co = oct * 4;
 
     for (int k = tid; k < K; k += KA_THREADS) s_cnt[k] = 0;
-    if (CFULL) {
-        for (int64_t t = tid; t < (int64_t)Kp * d; t += KA_THREADS) {
-            const int k = (int)(t / d), c = (int)(t % d);
-            Cs[k * dp + c] = k < K ? C[(int64_t)k * ldc + c] : 0.0;
+    auto stage_c = [&](int k_first, int k_count) {
+        for (int t = tid; t < k_count * d; t += KA_THREADS) {
+            const int k = t / d, c = t % d;
+            Cs[k * G.rs + G.pos(c)] = k_first + k < K ? C[(int64_t)(k_first + k) * ldc + c] : 0.0;
         }
-    }
-    unsigned long long n_changed = 0;
-
-    for (int64_t row0 = (int64_t)blockIdx.x * KA_TM; row0 < n; row0 += (int64_t)gridDim.x * KA_TM) {
-        __syncthreads();  // previous tile consumed (and CFULL staging / counters visible)
+    };
+    if (CFULL) stage_c(0, Kp);
+    auto stage_x = [&](double *dst, int64_t r0) {
         for (int t = tid; t < KA_TM * d; t += KA_THREADS) {
             const int r = t / d, c = t % d;
-            const int64_t gr = row0 + r;
-            Xs[r * dp + c] = gr < n ? X[gr * ld + c] : 0.0;
+            const int64_t gr = r0 + r;
+            ca8(dst + r * G.rs + G.pos(c), X + (gr < n ? gr : 0) * ld + c, gr < n ? 8 : 0);
         }
-        double bd[4];
-        int bk[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) bd[i] = CUDART_INF, bk[i] = INT32_MAX;
+        ca_commit();
+    };
+    unsigned long long n_changed = 0;
+    const int64_t stride = (int64_t)gridDim.x * KA_TM;
+    int buf = 0;
+    if ((int64_t)blockIdx.x * KA_TM < n) stage_x(Xb, (int64_t)blockIdx.x * KA_TM);
+
+    for (int64_t row0 = (int64_t)blockIdx.x * KA_TM; row0 < n; row0 += stride, buf ^= 1) {
+        __syncthreads();  // previous tile consumed (CFULL staging, counters and candidates visible)
+        if (row0 + stride < n)
+            stage_x(Xb + (buf ^ 1) * KA_TM * G.rs, row0 + stride);
+        else
+            ca_commit();  // empty group keeps the wait count uniform
+        ca_wait<1>();
+        __syncthreads();
+        const double *xr = Xb + buf * KA_TM * G.rs + rq * G.rs;
+        // after the transpose-reduce below, lane j holds row mi = 2 b0 + b1 of
+        // its quad and centroids 2 b2 + {0, 1} of its quartet
+        const int b0 = j & 1, b1 = (j >> 1) & 1, b2 = (j >> 2) & 1;
+        const int mi = 2 * b0 + b1;
+        const double xim = row0 + rq + mi < n ? xx[row0 + rq + mi] : 0.0;
+        double bd = CUDART_INF;
+        int bk = INT32_MAX;
 
         for (int k0 = 0; k0 < K; k0 += KA_TK) {
             const double *Ct = Cs;
             if (!CFULL) {
                 __syncthreads();
-                for (int t = tid; t < KA_TK * d; t += KA_THREADS) {
-                    const int k = t / d, c = t % d;
-                    Cs[k * dp + c] = k0 + k < K ? C[(int64_t)(k0 + k) * ldc + c] : 0.0;
+                stage_c(k0, KA_TK);
+                __syncthreads();
+            } else {
+                Ct = Cs + (int64_t)k0 * G.rs;
+            }
+            if (k0 + co >= K) continue;  // whole quartet past K (warp-uniform)
+            const double *cr = Ct + co * G.rs;
+            double dot[2];
+            if (T > 0) {
+                double acc[4][4];
+                const double *xj = xr + j * G.tp, *cj = cr + j * G.tp;
+                // body: first step peeled (r[j] starts at the first product), then
+                // pairs of steps per 16-byte load, the odd last step peeled
+                {
+                    double2 xv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xj + i * G.rs);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 cv = *reinterpret_cast<const double2 *>(cj + q * G.rs);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[i][q] = __dmul_rn(xv[i].x, cv.x);
+                    }
+                    if (T > 1) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const double cy = cj[q * G.rs + 1];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i].y, cy));
+                        }
+                    }
+                }
+                int t = 2;
+                for (; t + 1 < T; t += 2) {
+                    double2 xv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xj + i * G.rs + t);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double2 cv = *reinterpret_cast<const double2 *>(cj + q * G.rs + t);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i].x, cv.x));
+                            acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i].y, cv.y));
+                        }
+                    }
+                }
+                if (t < T) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double cx = cj[q * G.rs + t];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xj[i * G.rs + t], cx));
+                    }
+                }
+                // transpose-reduce over the 8 residue lanes in numpy's tree order
+                // (xor 1, 2, 4 = (r0+r1), (r01+r23), (r0123+r4567)); each round keeps
+                // the half of the (row, centroid) pairs selected by one lane bit
+                double r1[8], r2[4];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {  // pair (i, q) = (2 * bit + (e >> 2), e & 3)
+                    const double lo = acc[e >> 2][e & 3], hi = acc[2 + (e >> 2)][e & 3];
+                    r1[e] = __dadd_rn(b0 ? hi : lo, __shfl_xor_sync(0xffffffffu, b0 ? lo : hi, 1));
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {  // row bit 0
+                    const double lo = r1[e], hi = r1[4 + e];
+                    r2[e] = __dadd_rn(b1 ? hi : lo, __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2));
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {  // centroid bit 1
+                    const double lo = r2[e], hi = r2[2 + e];
+                    dot[e] = __dadd_rn(b2 ? hi : lo, __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4));
                 }
             } else {
-                Ct = Cs + (int64_t)k0 * dp;
+                dot[0] = dot[1] = -0.0;  // numpy: rows shorter than 8 sum from -0.0
             }
-            __syncthreads();
-            const double *xr = Xs + rq * dp;
-            const double *cr = Ct + co * dp;
-            double acc[4][8];
-            if (d >= 8) {
+            const double *xm = xr + mi * G.rs;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) acc[i][q] = __dmul_rn(xr[i * dp + j], cr[q * dp + j]);
-                for (int c = 8 + j; c < body; c += 8) {
-                    double xv[4], cv[8];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[i] = xr[i * dp + c];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) cv[q] = cr[q * dp + c];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i], cv[q]));
+            for (int e = 0; e < 2; ++e) {
+                const int q = 2 * b2 + e;
+                for (int c = G.body; c < d; ++c) {  // tail, in order
+                    const int pc = 8 * G.tp + (c - G.body);
+                    dot[e] = __dadd_rn(dot[e], __dmul_rn(xm[pc], cr[q * G.rs + pc]));
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) acc[i][q] = tree8(acc[i][q]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) acc[i][q] = -0.0;
-            }
-            for (int c = body; c < d; ++c) {  // tail, in order (all lanes alike)
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xr[i * dp + c], cr[q * dp + c]));
-            }
-            // epilogue of this centroid tile: every lane of the group holds all 32 dots
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t row = row0 + rq + i;
-                const double xi = row < n ? xx[row] : 0.0;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = k0 + co + q;
-                    if (k < K) lexmin(bd[i], bk[i], np_max0(__dsub_rn(__dadd_rn(xi, cc[k]), 2.0 * acc[i][q])), k);
+                const int k = k0 + co + q;
+                if (k < K) {
+                    double v = __dsub_rn(__dadd_rn(xim, cc[k]), __dadd_rn(dot[e], dot[e]));
+                    v = v < 0.0 ? 0.0 : v;  // np.maximum(v, 0.0): keeps NaN and -0.0
+                    if (v < bd) bd = v, bk = k;  // ascending k: first minimum
                 }
-                // merge the 4 groups of the warp (lane offsets 8 and 16)
-                lexmin(bd[i], bk[i], __shfl_xor_sync(0xffffffffu, bd[i], 8), __shfl_xor_sync(0xffffffffu, bk[i], 8));
-                lexmin(bd[i], bk[i], __shfl_xor_sync(0xffffffffu, bd[i], 16), __shfl_xor_sync(0xffffffffu, bk[i], 16));
             }
         }
-        if ((g & 3) == 0 && j < 4) {  // lane j of the warp's first group writes row rq + j
-            double v = bd[0];
-            int k = bk[0];
+        // lanes j and j^4 share a row (different centroid pairs)
+        lexmin(bd, bk, __shfl_xor_sync(0xffffffffu, bd, 4), __shfl_xor_sync(0xffffffffu, bk, 4));
+        if (b2 == 0) cand_d[oct * KA_TM + rq + mi] = bd, cand_k[oct * KA_TM + rq + mi] = bk;
+
+        // merge the four quartet warps of each row (lexicographic (d2, k): first minimum)
+        __syncthreads();
+        if (tid < KA_TM) {
+            const int64_t row = row0 + tid;
+            double v = cand_d[tid];
+            int k = cand_k[tid];
 #pragma unroll
-            for (int i = 1; i < 4; ++i)
-                if (j == i) v = bd[i], k = bk[i];
-            const int64_t row = row0 + rq + j;
+            for (int o = 1; o < 4; ++o) lexmin(v, k, cand_d[o * KA_TM + tid], cand_k[o * KA_TM + tid]);
             if (row < n) {
                 if (k == INT32_MAX) k = 0;  // all distances NaN: np.argmin returns 0
                 n_changed += lab_old[row] != k;
@@ -475,29 +624,59 @@ __global__ void __launch_bounds__(256) k_km_seg_hist(const int *__restrict__ lab
     for (int k = threadIdx.x; k < K; k += blockDim.x) seg_off[(int64_t)blockIdx.x * K + k] = s_h[k];
 }
 
-// seg_off[s][k] <- start[k] + sum_{s' < s} count[s'][k];  start = exclusive scan of totals
-__global__ void k_km_seg_scan(int64_t *__restrict__ seg_off, int64_t nseg, int K, int64_t *__restrict__ start) {
-    for (int k = threadIdx.x; k < K; k += blockDim.x) {
-        int64_t t = 0;
-        for (int64_t s = 0; s < nseg; ++s) {
-            const int64_t c = seg_off[s * K + k];
-            seg_off[s * K + k] = t;
-            t += c;
+// seg_off[s][k] <- sum_{s' < s} count[s'][k] (one warp per label, shuffle scan
+// over 32 segments at a time); tot[k] = the label's row count
+__global__ void __launch_bounds__(256) k_km_seg_scan(int64_t *__restrict__ seg_off, int64_t nseg, int K,
+                                                     int64_t *__restrict__ tot) {
+    const int lane = threadIdx.x & 31;
+    const int k = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (k >= K) return;
+    int64_t run = 0;
+    for (int64_t s0 = 0; s0 < nseg; s0 += 32) {
+        const int64_t s = s0 + lane;
+        const int64_t c = s < nseg ? seg_off[s * K + k] : 0;
+        int64_t inc = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
         }
-        start[k + 1] = t;  // totals, scanned below
+        if (s < nseg) seg_off[s * K + k] = run + inc - c;
+        run += __shfl_sync(0xffffffffu, inc, 31);
     }
+    if (lane == 0) tot[k] = run;
+}
+
+// start[0] = 0, start[k + 1] = start[k] + tot[k] (one block; thread t owns a
+// contiguous run of labels)
+__global__ void __launch_bounds__(1024) k_km_start_scan(const int64_t *__restrict__ tot, int K,
+                                                        int64_t *__restrict__ start) {
+    __shared__ int64_t part[1024];
+    const int per = (K + blockDim.x - 1) / blockDim.x;
+    const int lo = min(K, (int)threadIdx.x * per), hi = min(K, lo + per);
+    int64_t s = 0;
+    for (int k = lo; k < hi; ++k) s += tot[k];
+    part[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
-        start[0] = 0;
-        for (int k = 0; k < K; ++k) start[k + 1] += start[k];
+        int64_t run = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int64_t v = part[t];
+            part[t] = run;
+            run += v;
+        }
+        start[K] = run;
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < K; k += blockDim.x)
-        for (int64_t s = 0; s < nseg; ++s) seg_off[s * K + k] += start[k];
+    int64_t run = part[threadIdx.x];
+    for (int k = lo; k < hi; ++k) {
+        start[k] = run;
+        run += tot[k];
+    }
 }
 
 __global__ void k_km_seg_scatter(const int *__restrict__ lab, int64_t n, int K, int64_t seg,
-                                 int64_t *__restrict__ seg_off, int64_t *__restrict__ order) {
+                                 int64_t *__restrict__ seg_off, const int64_t *__restrict__ start,
+                                 int64_t *__restrict__ order) {
     const int lane = threadIdx.x & 31;
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int64_t lo = s * seg, hi = min(n, lo + seg);
@@ -510,39 +689,63 @@ __global__ void k_km_seg_scatter(const int *__restrict__ lab, int64_t n, int K, 
         const int l = live ? lab[i] : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, l);
         const int rank = __popc(peers & lt);
-        if (live) order[off[l] + rank] = i;
+        if (live) order[start[l] + off[l] + rank] = i;
         __syncwarp();
         if (live && rank == 0) off[l] += __popc(peers);
         __syncwarp();
     }
 }
 
-// C[k][col] = (sum over the cluster's rows in row order) / count   (cluster.py:98-100)
-__global__ void __launch_bounds__(256) k_km_sums(const double *__restrict__ X, int d, int64_t ld,
-                                                 const int64_t *__restrict__ order, const int64_t *__restrict__ start,
-                                                 int K, double *__restrict__ C, int64_t ldc) {
-    const int lane = threadIdx.x & 31;
+// C[k][col] = (sum over the cluster's rows in row order) / count   (cluster.py:98-100).
+// One warp (block) per (cluster, 32-column slice), lane = column.  The adds are
+// a sequential chain in row order, so the rows are streamed ahead through a
+// per-warp ring of KS_D 32-row batches in shared memory (8-byte cp.async per
+// lane and row, zero-filled past the cluster / the row width); row indices
+// are loaded one batch ahead of their copies.
+constexpr int KS_D = 8;
+
+__global__ void __launch_bounds__(32) k_km_sums(const double *__restrict__ X, int d, int64_t ld,
+                                                const int64_t *__restrict__ order, const int64_t *__restrict__ start,
+                                                int K, double *__restrict__ C, int64_t ldc) {
+    extern __shared__ double ring[];  // [KS_D][32 rows][32 lanes]
+    const int lane = threadIdx.x;
     const int slices = (d + 31) / 32;
-    const int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (w >= (int64_t)K * slices) return;
-    const int k = (int)(w / slices);
-    const int col = (int)(w % slices) * 32 + lane;
+    const int k = blockIdx.x / slices;
+    const int col = (blockIdx.x % slices) * 32 + lane;
     const bool live = col < d;
     const int64_t b = start[k], e = start[k + 1];
-    double acc = 0.0;
-    for (int64_t j = b; j < e; j += 32) {
-        const int cnt = (int)min((int64_t)32, e - j);
-        const int64_t my = lane < cnt ? order[j + lane] : 0;
-        double v[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const int64_t r = __shfl_sync(0xffffffffu, my, t);
-            v[t] = (live && t < cnt) ? X[r * ld + col] : 0.0;
+    const int64_t nb = (e - b + 31) / 32;
+    auto index_of = [&](int64_t bi) -> int64_t {
+        const int64_t j = b + bi * 32 + lane;
+        return (bi < nb && j < e) ? order[j] : 0;
+    };
+    auto issue = [&](int64_t bi, int64_t my) {
+        if (bi < nb) {
+            const int cnt = (int)min((int64_t)32, e - (b + bi * 32));
+            double *slot = ring + (bi % KS_D) * 1024;
+#pragma unroll 8
+            for (int t = 0; t < 32; ++t) {
+                const int64_t r = __shfl_sync(0xffffffffu, my, t);
+                ca8(slot + t * 32 + lane, X + r * ld + (live ? col : 0), (live && t < cnt) ? 8 : 0);
+            }
         }
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-            if (t < cnt) acc = __dadd_rn(acc, v[t]);
+        ca_commit();  // possibly empty: one group per batch slot keeps the wait count uniform
+    };
+    for (int bi = 0; bi < KS_D - 1; ++bi) issue(bi, index_of(bi));
+    int64_t my_next = index_of(KS_D - 1);
+    double acc = 0.0;
+    for (int64_t bi = 0; bi < nb; ++bi) {
+        const int64_t my = my_next;
+        my_next = index_of(bi + KS_D);
+        issue(bi + KS_D - 1, my);
+        ca_wait<KS_D - 1>();
+        __syncwarp();
+        const int cnt = (int)min((int64_t)32, e - (b + bi * 32));
+        const double *slot = ring + (bi % KS_D) * 1024;
+        for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, slot[t * 32 + lane]);
+        __syncwarp();  // slot free for batch bi + KS_D
     }
+    ca_wait<0>();
     if (live) C[(int64_t)k * ldc + col] = __ddiv_rn(acc, (double)(e - b));
 }
 

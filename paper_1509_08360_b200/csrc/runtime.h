@@ -36,7 +36,13 @@ struct csemb_ctx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     std::mutex mu;
+    void *scratch = nullptr;  // grow-only device scratch for per-call temporaries
+    size_t scratch_bytes = 0;
 };
+
+// the context's scratch buffer with at least `bytes` (call with c->mu held;
+// valid until the next call that grows it)
+CSEMB_INTERNAL cudaError_t ctx_scratch(csemb_ctx *c, size_t bytes, void **out);
 
 // Load-balance schedule of a matrix for one group width G (see K1c in kernels.cuh):
 // rows longer than `threshold` are cut into chunks of `chunk` entries (heavy);
