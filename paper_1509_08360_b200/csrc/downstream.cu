@@ -398,10 +398,10 @@ extern "C" int csemb_modularity_counts(csemb_mat *m, const int32_t *labels, int 
     cudaStream_t s = c->stream;
     int *dl = nullptr;
     unsigned long long *cnt = nullptr;
-    cudaError_t e = cudaMalloc(&cnt, 16 * (size_t)k);
+    cudaError_t e = cudaMalloc(&cnt, 16 * (size_t)k + 8);  // [k] intra2, [k] degsum, bad-label count
     if (e == cudaSuccess && !on_device) e = cudaMalloc(&dl, 4 * std::max<int64_t>(n, 1));
     if (e == cudaSuccess && !on_device && n) e = cudaMemcpyAsync(dl, labels, 4 * n, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 16 * (size_t)k, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 16 * (size_t)k + 8, s);
     if (e == cudaSuccess && n) {
         const int *lab = on_device ? labels : dl;
         const size_t smem = 16 * (size_t)k;
@@ -410,18 +410,19 @@ extern "C" int csemb_modularity_counts(csemb_mat *m, const int32_t *labels, int 
             if (smem > 48 * 1024)
                 e = cudaFuncSetAttribute(k_modularity<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e == cudaSuccess)
-                k_modularity<true><<<g, 256, smem, s>>>(m->rowptr, m->cols, n, lab, (int)k, cnt, cnt + k);
+                k_modularity<true><<<g, 256, smem, s>>>(m->rowptr, m->cols, n, lab, (int)k, cnt, cnt + k, cnt + 2 * k);
         } else {
-            k_modularity<false><<<g, 256, 0, s>>>(m->rowptr, m->cols, n, lab, (int)k, cnt, cnt + k);
+            k_modularity<false><<<g, 256, 0, s>>>(m->rowptr, m->cols, n, lab, (int)k, cnt, cnt + k, cnt + 2 * k);
         }
         if (e == cudaSuccess) e = cudaGetLastError();
     }
-    std::vector<unsigned long long> h(2 * (size_t)k);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), cnt, 16 * (size_t)k, cudaMemcpyDeviceToHost, s);
+    std::vector<unsigned long long> h(2 * (size_t)k + 1);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), cnt, 16 * (size_t)k + 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaFree(dl);
     cudaFree(cnt);
     CK(e);
+    if (h[2 * k]) return fail(CSEMB_ERR_INVALID, "%llu labels outside [0, %lld)", h[2 * k], (long long)k);
     for (int64_t q = 0; q < k; ++q) {
         intra[q] = (int64_t)(h[q] / 2);  // each intra edge is stored as (u, v) and (v, u)
         degsum[q] = (int64_t)h[k + q];

@@ -761,7 +761,8 @@ template <bool SMEM_HIST>
 __global__ void __launch_bounds__(256) k_modularity(const int64_t *__restrict__ rowptr, const int *__restrict__ cols,
                                                     int64_t n, const int *__restrict__ lab, int K,
                                                     unsigned long long *__restrict__ intra2,
-                                                    unsigned long long *__restrict__ degsum) {
+                                                    unsigned long long *__restrict__ degsum,
+                                                    unsigned long long *__restrict__ bad) {
     extern __shared__ unsigned long long s_m[];  // [K] intra2, [K] degsum
     if (SMEM_HIST) {
         for (int k = threadIdx.x; k < 2 * K; k += blockDim.x) s_m[k] = 0;
@@ -770,6 +771,10 @@ __global__ void __launch_bounds__(256) k_modularity(const int64_t *__restrict__ 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int l = lab[i];
+        if (l < 0 || l >= K) {  // caller-supplied device labels: flag, never index out of range
+            atomicAdd(bad, 1ull);
+            continue;
+        }
         const int64_t b = rowptr[i], e = rowptr[i + 1];
         unsigned long long same = 0;
         for (int64_t q = b; q < e; ++q) same += lab[cols[q]] == l;

@@ -225,3 +225,21 @@ def test_cluster_experiment_matches_reference(ds):
     assert np.array_equal(ex.median_labels, z["experiment_median_labels"])
     with pytest.raises(ValueError):
         pcl.cluster_experiment(c1["edges"], 2000, pb.indicator_above(0.9), pb.EmbedConfig(L=60, d=40), K=4, runs=0)
+
+
+def test_modularity_rejects_bad_device_labels(config1):
+    """Device-resident labels outside [0, k) are reported, never used as indices."""
+    import torch
+
+    c1, _ = config1
+    dm = pb.DeviceMatrix(sparse_from(c1), "float64")
+    lab = torch.zeros(2000, dtype=torch.int32, device="cuda")
+    lab[17] = 9
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError):
+        pcl.modularity_counts(dm, lab.data_ptr(), 4)
+    lab[17] = 3
+    torch.cuda.synchronize()
+    intra, degsum = pcl.modularity_counts(dm, lab.data_ptr(), 4)
+    assert degsum.sum() == dm.nnz
+    dm.close()
