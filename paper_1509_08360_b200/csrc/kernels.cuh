@@ -43,6 +43,11 @@ template <> struct Vec<float> {
 __device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0); }
 __device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
+#ifndef K1_PREFETCH
+#define K1_PREFETCH 1  // L2 prefetch of the epilogue's streamed rows at the start of each row set (fp64)
+#endif
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // acc + a*x, separately rounded (fp64 strict) / fused (fp32)
 #ifndef K1_FMA64
 #define K1_FMA64 0  // 1: fused multiply-add in fp64 (not bit-identical to the reference; experiment)
@@ -391,6 +396,24 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         const int len = (int)(end - beg);
         const int nb_mine = (len + B - 1) / B;
         const int nb = __reduce_max_sync(0xFFFFFFFFu, (unsigned)nb_mine);
+#if K1_PREFETCH
+        // the epilogue's streamed rows (Q(r-2), E, own Q(r-1)) are requested into
+        // L2 now, so the loads after the gather loop hit L2 instead of DRAM
+        // (fp64 only: measured -2.5% on config 2 f64, +5% on the issue-bound f32 tiles)
+        if (MODE == MODE_RECUR && sizeof(T) == 8 && active) {
+            const VT *pq = yout + row * (int64_t)P.ldv + P.v0 + gl;
+            const VT *pe = E + row * (int64_t)P.ldv + P.v0 + gl;
+            const VT *po = ycur + (P.row_base + row) * (int64_t)P.ldv;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                if (valid[k]) {
+                    if (has_prev) prefetch_l2(pq + k * G);
+                    if (P.efold) prefetch_l2(pe + k * G);
+                    if (P.efold & 2) prefetch_l2(po + k * G);
+                }
+            }
+        }
+#endif
 
         VT acc[VPL];
 #pragma unroll
