@@ -108,8 +108,11 @@ int csemb_plan_destroy(csemb_plan *p);
 #define CSEMB_OPT_SPLIT_THRESHOLD 3 /* rows longer than this (default 4096) are split
                                        into 1024-entry chunks summed in chunk order;
                                        0 = never split (bit-exact for every input) */
-#define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default), 0 natural, 1 bucketed by
-                                       batch count (skewed row lengths) */
+#define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default: 1 for skewed row lengths,
+                                       else 2), 0 natural, 1 bucketed by batch count,
+                                       2 bucketed within windows of consecutive rows
+                                       (window chosen against the grid's wave), >= 64:
+                                       that window.  Row order never changes results. */
 #define CSEMB_OPT_E_FOLD 5           /* 1..3 (default 3): E is read and written every
                                        e_fold steps; a flush adds the pending terms in
                                        the reference's order, so results are unchanged */

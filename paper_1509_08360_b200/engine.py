@@ -249,7 +249,8 @@ class Plan:
         """Rows longer than split_threshold (default 4096; 0 = never) are split
         into chunks summed in chunk order (no longer bit-identical to the
         reference's sequential sum for those rows); row_order -1 auto /
-        0 natural / 1 bucketed by length.  Reordering never changes results."""
+        0 natural / 1 bucketed by length / 2 bucketed within windows of
+        consecutive rows / >= 64 that window.  Reordering never changes results."""
         if split_threshold is not None:
             self.set_option(_lib.OPT_SPLIT_THRESHOLD, int(split_threshold))
         if row_order is not None:

@@ -277,6 +277,11 @@ class TestEdgeCases:
         assert np.array_equal(plan.apply(th, 1, om), ref)
         plan.set_load_balance(row_order=0)
         assert np.array_equal(plan.apply(th, 1, om), ref)
+        for ro in (2, 64, 1000, 8192):  # windowed bucketing (auto window / explicit windows)
+            plan.set_load_balance(row_order=ro)
+            assert np.array_equal(plan.apply(th, 1, om), ref), ro
+        with pytest.raises(ValueError):
+            plan.set_load_balance(row_order=3)
         plan.set_load_balance(split_threshold=64, row_order=-1)
         got = plan.apply(th, 1, om)
         assert rel(got, ref) <= 1e-13

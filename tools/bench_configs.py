@@ -47,8 +47,13 @@ class CutAbove:
         return (self.c,)
 
 
+ROW_ORDER = None
+
+
 def run_embed(dm, coeffs, d, reps, dtype, normalize=True):
     plan = dm.plan(d)
+    if ROW_ORDER is not None:
+        plan.set_load_balance(row_order=ROW_ORDER)
     res = []
     for _ in range(reps + 1):
         plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7, normalize_rows=normalize)
@@ -118,7 +123,9 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="3,4")
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--row-order", type=int, default=None)
     args = ap.parse_args()
+    ROW_ORDER = args.row_order
     for c in args.configs.split(","):
         {"3": config3, "4": config4}[c](args)
         torch.cuda.empty_cache()

@@ -27,6 +27,7 @@ ap.add_argument("--graphs", default="band,sbm,random")
 ap.add_argument("--widths", default="80")
 ap.add_argument("--efold", type=int, default=None)
 ap.add_argument("--reverse", type=int, default=None)
+ap.add_argument("--row-order", type=int, default=None, help="-1 auto, 0 natural, 1 bucketed by batch count")
 args = ap.parse_args()
 n = args.n
 
@@ -51,6 +52,8 @@ for name in args.graphs.split(","):
             plan.set_option(_lib.OPT_E_FOLD, args.efold)
         if args.reverse is not None:
             plan.set_option(_lib.OPT_REVERSE_SWEEP, args.reverse)
+        if args.row_order is not None:
+            plan.set_option(_lib.OPT_ROW_ORDER, args.row_order)
         best = 1e9
         for _ in range(3):
             plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
