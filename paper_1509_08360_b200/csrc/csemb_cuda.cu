@@ -327,11 +327,25 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
         }
     }
     const bool bucket = order == 1 || window > 0 || (order < 0 && skewed);
-    if (window > 0) {
-        auto key = [&](int r) { return (rp[r + 1] - rp[r] + G - 1) / G; };
+    if (window > 0) {  // stable counting sort by batch count inside each window
+        const int64_t cap = 1 << 16;
+        std::vector<int> key(light.size());
+        int kmax = 0;
+        for (size_t i = 0; i < light.size(); ++i) {
+            const int r = light[i];
+            key[i] = (int)std::min<int64_t>((rp[r + 1] - rp[r] + G - 1) / G, cap);
+            kmax = std::max(kmax, key[i]);
+        }
+        std::vector<int64_t> cnt((size_t)kmax + 2);
+        std::vector<int> tmp;
         for (size_t w0 = 0; w0 < light.size(); w0 += (size_t)window) {
             const size_t w1 = std::min(light.size(), w0 + (size_t)window);
-            std::stable_sort(light.begin() + w0, light.begin() + w1, [&](int x, int y) { return key(x) < key(y); });
+            std::fill(cnt.begin(), cnt.end(), 0);
+            for (size_t i = w0; i < w1; ++i) ++cnt[(size_t)key[i] + 1];
+            for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+            tmp.resize(w1 - w0);
+            for (size_t i = w0; i < w1; ++i) tmp[(size_t)cnt[(size_t)key[i]]++] = light[i];
+            std::copy(tmp.begin(), tmp.end(), light.begin() + w0);
         }
     } else if (bucket) {  // stable counting sort of the light rows by batch count
         const int64_t cap = 1 << 16;
