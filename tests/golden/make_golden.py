@@ -418,6 +418,48 @@ def gen_downstream():
     _save("downstream", meta, **arrays)
 
 
+def gen_cli_downstream():
+    """The reference CLI's `cluster` and `eval` commands (cli.py:226-281) on a
+    small SBM edge list: cluster summary JSON + labels CSV; eval's percentile /
+    calibration CSVs and report JSON for an embedding from its own `embed`."""
+    import tempfile
+
+    from csemb.cli import main
+
+    edges, _ = sbm(300, 3, 0.2, 0.01, np.random.default_rng(41))
+    arrays, meta = {"edges": edges.astype(np.int64)}, {}
+    with tempfile.TemporaryDirectory() as tmp:
+        g = os.path.join(tmp, "g.txt")
+        with open(g, "w") as fh:
+            fh.write("\n".join(f"{u} {v}" for u, v in edges) + "\n")
+        cl = ["cluster", "--input", g, "--function", "indicator:0.5", "--L", "40", "--d", "24", "--seed", "5",
+              "--k", "3", "--runs", "5"]
+        lab, summ = os.path.join(tmp, "labels.csv"), os.path.join(tmp, "summary.json")
+        assert main(cl + ["--labels-out", lab, "--summary-out", summ]) == 0
+        meta["cluster"] = {"argv": cl, "summary": json.load(open(summ))}
+        meta["cluster"]["summary"].pop("input")
+        arrays["cluster_labels_csv"] = np.frombuffer(open(lab, "rb").read(), dtype=np.uint8)
+        emb = os.path.join(tmp, "e.bin")
+        em = ["embed", "--input", g, "--format", "edgelist", "--function", "indicator:0.5", "--L", "40",
+              "--d", "24", "--seed", "5", "--output", emb]
+        assert main(em) == 0
+        arrays["eval_approx"] = cio_read(emb)
+        ev = ["eval", "--approx", emb, "--input", g, "--format", "edgelist", "--function", "indicator:0.5",
+              "--pairs", "5000", "--seed", "2", "--output-prefix", os.path.join(tmp, "ev")]
+        assert main(ev) == 0
+        meta["eval"] = {"argv_tail": ev[3:], "report": json.load(open(os.path.join(tmp, "ev_report.json")))}
+        for part in ("percentiles", "calibration"):
+            arrays[f"eval_{part}_csv"] = np.frombuffer(open(os.path.join(tmp, f"ev_{part}.csv"), "rb").read(),
+                                                       dtype=np.uint8)
+    _save("cli_downstream", meta, **arrays)
+
+
+def cio_read(path):
+    from csemb import io as cio
+
+    return cio.read_embedding(path)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -431,3 +473,4 @@ if __name__ == "__main__":
     gen_builders()
     gen_cli()
     gen_downstream()
+    gen_cli_downstream()

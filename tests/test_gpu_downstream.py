@@ -243,3 +243,83 @@ def test_modularity_rejects_bad_device_labels(config1):
     intra, degsum = pcl.modularity_counts(dm, lab.data_ptr(), 4)
     assert degsum.sum() == dm.nnz
     dm.close()
+
+
+@pytest.fixture(scope="module")
+def cd():
+    return load_golden("cli_downstream")
+
+
+class TestCLIDownstream:
+    """The reference CLI's `cluster` / `eval` commands on the device, against
+    the reference CLI's own outputs (tests/golden/cli_downstream.npz)."""
+
+    def _graph(self, cd, tmp_path):
+        z, _ = cd
+        g = tmp_path / "g.txt"
+        g.write_text("\n".join(f"{u} {v}" for u, v in z["edges"]) + "\n")
+        return str(g)
+
+    def test_cluster(self, cd, tmp_path):
+        import json
+
+        from paper_1509_08360_b200 import cli
+
+        z, meta = cd
+        argv = list(meta["cluster"]["argv"])
+        argv[argv.index("--input") + 1] = self._graph(cd, tmp_path)
+        lab, summ = tmp_path / "labels.csv", tmp_path / "summary.json"
+        assert cli.main(argv + ["--labels-out", str(lab), "--summary-out", str(summ)]) == 0
+        got = json.load(open(summ))
+        got.pop("input")
+        assert got == meta["cluster"]["summary"]
+        assert lab.read_bytes() == bytes(z["cluster_labels_csv"])
+
+    def test_eval(self, cd, tmp_path):
+        import csv
+        import json
+
+        from paper_1509_08360_b200 import cli
+        from paper_1509_08360_b200 import io as pio
+
+        z, meta = cd
+        approx = tmp_path / "e.bin"
+        pio.write_embedding(str(approx), z["eval_approx"])
+        g = self._graph(cd, tmp_path)
+        argv = ["eval", "--approx", str(approx), "--input", g] + meta["eval"]["argv_tail"][2:]
+        pref = str(tmp_path / "ev")
+        argv[argv.index("--output-prefix") + 1] = pref
+        assert cli.main(argv) == 0
+        rep, want = json.load(open(pref + "_report.json")), meta["eval"]["report"]
+        assert (rep["pair_sample_size"], rep["zero_row_pairs"]) == (want["pair_sample_size"], want["zero_row_pairs"])
+        for k, v in want["percentiles"].items():
+            assert abs(rep["percentiles"][k] - v) <= 1e-10
+        for part in ("percentiles", "calibration"):
+            got = list(csv.reader(open(f"{pref}_{part}.csv")))
+            ref = list(csv.reader(bytes(z[f"eval_{part}_csv"]).decode().splitlines()))
+            assert got[0] == ref[0] and len(got) == len(ref)
+            for gr, rr in zip(got[1:], ref[1:]):
+                assert np.allclose([float(x) for x in gr], [float(x) for x in rr], rtol=0, atol=1e-10)
+        # the same report from a precomputed exact embedding file
+        ex = D.exact_embedding(pb.normalized_adjacency(z["edges"], 300).to_dense(), pb.indicator_above(0.5))
+        exf = tmp_path / "exact.bin"
+        pio.write_embedding(str(exf), ex.embedding)
+        argv2 = ["eval", "--approx", str(approx), "--exact", str(exf), "--pairs", "5000", "--seed", "2",
+                 "--output-prefix", pref + "2"]
+        assert cli.main(argv2) == 0
+        rep2 = json.load(open(pref + "2_report.json"))
+        for k, v in want["percentiles"].items():
+            assert abs(rep2["percentiles"][k] - v) <= 1e-10
+
+    def test_eval_cap_exit_code(self, tmp_path):
+        from paper_1509_08360_b200 import cli
+        from paper_1509_08360_b200 import io as pio
+
+        n = 3001
+        g = tmp_path / "big.txt"
+        g.write_text("\n".join(f"{i} {i + 1}" for i in range(n - 1)) + "\n")
+        approx = tmp_path / "a.bin"
+        pio.write_embedding(str(approx), np.ones((n, 4)))
+        rc = cli.main(["eval", "--approx", str(approx), "--input", str(g), "--format", "edgelist", "--function",
+                       "indicator:0.5", "--output-prefix", str(tmp_path / "x")])
+        assert rc == 5

@@ -252,3 +252,21 @@ class TestIOAndCLI:
         g.write_text("zero one\n")
         assert main(["embed", "--input", str(g), "--format", "edgelist", "--function", "indicator:0.5", "--L", "4",
                      "--output", str(tmp_path / "o.bin")]) == 3
+
+
+def test_cli_downstream_commands_parse_and_usage_errors(tmp_path):
+    """`cluster` / `eval` exist with the reference's options; eval without an
+    exact source is a usage error (exit 2), before any device work."""
+    from paper_1509_08360_b200 import cli, io as pio
+
+    p = cli.build_parser()
+    a = p.parse_args(["cluster", "--input", "g.txt", "--function", "indicator:0.5", "--L", "40"])
+    assert (a.k, a.runs, a.b, a.dtype) == (200, 25, 1, "float64")
+    e = tmp_path / "e.bin"
+    pio.write_embedding(str(e), np.ones((3, 2)))
+    with pytest.raises(SystemExit) as ex:
+        cli.main(["eval", "--approx", str(e), "--output-prefix", str(tmp_path / "o")])
+    assert ex.value.code == 2
+    with pytest.raises(SystemExit) as ex:
+        cli.main(["cluster", "--input", "g.txt", "--function", "indicator:0.5", "--L", "40", "--b", "3"])
+    assert ex.value.code == 2
