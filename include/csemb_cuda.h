@@ -113,6 +113,11 @@ int csemb_plan_destroy(csemb_plan *p);
                                        2 bucketed within windows of consecutive rows
                                        (window chosen against the grid's wave), >= 64:
                                        that window.  Row order never changes results. */
+#define CSEMB_OPT_GRAPH 6           /* -1 auto (default: blocks of <= 2^22 elements, where
+                                       launches dominate), 0 off, 1 on: the second
+                                       csemb_plan_run with an identical signature
+                                       (coefficients, options, block pointer, seed, slice)
+                                       is captured as a CUDA graph, later ones replay it */
 #define CSEMB_OPT_E_FOLD 5           /* 1..3 (default 3): E is read and written every
                                        e_fold steps; a flush adds the pending terms in
                                        the reference's order, so results are unchanged */

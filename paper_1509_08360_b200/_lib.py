@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("CSEMB_LIB_PATH") or os.path.join(_HERE, "libcsemb_cud
 OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_DIVERGED, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 OMEGA_GIVEN, OMEGA_SPLITMIX, OMEGA_PHILOX = 0, 1, 2
-OPT_EXACT_PEAKS, OPT_REVERSE_SWEEP, OPT_SPLIT_THRESHOLD, OPT_ROW_ORDER, OPT_E_FOLD = 1, 2, 3, 4, 5
+OPT_EXACT_PEAKS, OPT_REVERSE_SWEEP, OPT_SPLIT_THRESHOLD, OPT_ROW_ORDER, OPT_E_FOLD, OPT_GRAPH = 1, 2, 3, 4, 5, 6
 
 DIVERGENCE_MESSAGE = (
     "iteration r={r} produced non-finite values; the matrix likely has "

@@ -686,3 +686,30 @@ def test_fuzz_random_csr_bit_exact():
             assert np.array_equal(got, ref)
 
     check()
+
+
+def test_graph_replay_bit_exact(config1):
+    """CSEMB_OPT_GRAPH: the 2nd identical run is captured, later ones replay the
+    CUDA graph -- every run bit-identical to the reference, a changed signature
+    (seed, coefficients) re-captures, events still time the replay."""
+    z, meta = config1
+    S = sparse_from(z)
+    dm = pb.DeviceMatrix(S, "float64")
+    plan = dm.plan(40)
+    for mode in (1, 0, -1):
+        plan.set_option(pb._lib.OPT_GRAPH, mode)
+        for _ in range(4):
+            plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+            assert sha(plan.download()) == meta["E_sha256"]
+            tot, steps, launches = plan.timing()
+            assert tot > 0 and steps > 0 and launches == 60
+    other, _, _ = O.apply_expansion(O.CSR.of(S), z["coeffs"][:31], O.sample_projection(2000, 40, 3))
+    plan.set_option(pb._lib.OPT_GRAPH, 1)
+    for _ in range(3):
+        plan.run(z["coeffs"][:31], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=3)
+        assert np.array_equal(plan.download(), other)
+        plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+        assert sha(plan.download()) == meta["E_sha256"]
+    with pytest.raises(ValueError):
+        plan.set_option(pb._lib.OPT_GRAPH, 2)
+    dm.close()
