@@ -257,11 +257,12 @@ extern "C" int csemb_kmeans_assign(csemb_kmeans *k, double *inertia, int64_t *ch
     if (k->d <= KA_MAXD) {
         const KaGeom geo(k->d);
         const int Kp = (K + KA_TK - 1) / KA_TK * KA_TK;
-        const size_t base = 16 * (size_t)KA_TM * geo.rs + 12 * 4 * (size_t)KA_TM + 4 * (size_t)K;
+        const size_t base = 16 * (size_t)KA_TM * geo.rs + 12 * 4 * (size_t)KA_TM +
+                            (K <= KM_SMEM_K ? 4 * (size_t)K : 0);  // count histogram
         const size_t full = base + 8 * (size_t)Kp * geo.rs, tiled = base + 8 * (size_t)KA_TK * geo.rs;
         const bool cfull = full <= 220 * 1024;  // one 512-thread CTA per SM
         const size_t smem = cfull ? full : tiled;
-        if (smem > 220 * 1024) return fail(CSEMB_ERR_UNSUPPORTED, "K=%d exceeds the shared-memory histogram", K);
+        if (smem > 220 * 1024) return fail(CSEMB_ERR_UNSUPPORTED, "assignment tile does not fit shared memory");
         const void *fn = cfull ? (const void *)k_km_assign<true> : (const void *)k_km_assign<false>;
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const int g = (int)std::min<int64_t>(tiles, (int64_t)c->sm_count);
@@ -318,7 +319,7 @@ extern "C" int csemb_kmeans_commit(csemb_kmeans *k, int update_centroids) {
     std::swap(k->lab, k->lab_new);  // labels = new_labels
     if (update_centroids) {
         const int K = k->K;
-        const size_t hsmem = 4 * (size_t)K;
+        const size_t hsmem = K <= KM_SMEM_K ? 4 * (size_t)K : 0;
         if (hsmem > 48 * 1024)
             CK(cudaFuncSetAttribute(k_km_seg_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
         k_km_seg_hist<<<(unsigned)k->nseg, 256, hsmem, s>>>(k->lab, k->n, K, k->seg, k->seg_off);

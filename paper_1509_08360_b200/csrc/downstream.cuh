@@ -366,6 +366,7 @@ __global__ void k_km_reseed(const double *__restrict__ pv, const int64_t *__rest
 // store, #changed vs the previous labels, per-cluster counts.
 // ---------------------------------------------------------------------------
 constexpr int KA_TM = 64, KA_TK = 16, KA_THREADS = 512, KA_MAXD = 128;
+constexpr int KM_SMEM_K = 16384;  // above this many clusters, counts use global atomics
 
 // 8-byte async copy global -> shared (src_bytes 0 zero-fills), commit / wait
 __device__ __forceinline__ void ca8(double *dst, const double *src, int src_bytes) {
@@ -413,7 +414,9 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
     const int rq = (w >> 2) * 16 + ((tid >> 3) & 3) * 4;  // this group's 4 rows within the tile
     const int co = oct * 4;
 
-    for (int k = tid; k < K; k += KA_THREADS) s_cnt[k] = 0;
+    const bool scnt = K <= KM_SMEM_K;  // per-block shared histogram, else direct global counts
+    if (scnt)
+        for (int k = tid; k < K; k += KA_THREADS) s_cnt[k] = 0;
     auto stage_c = [&](int k_first, int k_count) {
         for (int t = tid; t < k_count * d; t += KA_THREADS) {
             const int k = t / d, c = t % d;
@@ -565,15 +568,19 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
                 n_changed += lab_old[row] != k;
                 lab_new[row] = k;
                 mind[row] = v;
-                atomicAdd(&s_cnt[k], 1u);
+                if (scnt)
+                    atomicAdd(&s_cnt[k], 1u);
+                else
+                    atomicAdd(&counts[k], 1ull);
             }
         }
     }
     for (int o = 16; o; o >>= 1) n_changed += __shfl_xor_sync(0xffffffffu, n_changed, o);
     if ((tid & 31) == 0 && n_changed) atomicAdd(changed, n_changed);
     __syncthreads();
-    for (int k = tid; k < K; k += KA_THREADS)
-        if (s_cnt[k]) atomicAdd(&counts[k], (unsigned long long)s_cnt[k]);
+    if (scnt)
+        for (int k = tid; k < K; k += KA_THREADS)
+            if (s_cnt[k]) atomicAdd(&counts[k], (unsigned long long)s_cnt[k]);
 }
 
 // d > 128 (several pairwise leaves): one 8-lane group per row, centroids in
@@ -616,12 +623,20 @@ __global__ void __launch_bounds__(256) k_km_assign_wide(
 __global__ void __launch_bounds__(256) k_km_seg_hist(const int *__restrict__ lab, int64_t n, int K, int64_t seg,
                                                      int64_t *__restrict__ seg_off) {
     extern __shared__ unsigned s_h[];
+    const int64_t lo = (int64_t)blockIdx.x * seg, hi = min(n, lo + seg);
+    int64_t *row = seg_off + (int64_t)blockIdx.x * K;
+    if (K > KM_SMEM_K) {  // large K: count straight into this segment's row
+        for (int k = threadIdx.x; k < K; k += blockDim.x) row[k] = 0;
+        __syncthreads();
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            atomicAdd(reinterpret_cast<unsigned long long *>(row + lab[i]), 1ull);
+        return;
+    }
     for (int k = threadIdx.x; k < K; k += blockDim.x) s_h[k] = 0;
     __syncthreads();
-    const int64_t lo = (int64_t)blockIdx.x * seg, hi = min(n, lo + seg);
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&s_h[lab[i]], 1u);
     __syncthreads();
-    for (int k = threadIdx.x; k < K; k += blockDim.x) seg_off[(int64_t)blockIdx.x * K + k] = s_h[k];
+    for (int k = threadIdx.x; k < K; k += blockDim.x) row[k] = s_h[k];
 }
 
 // seg_off[s][k] <- sum_{s' < s} count[s'][k] (one warp per label, shuffle scan

@@ -363,3 +363,15 @@ def test_fuzz_kmeans_modularity_cosines_vs_oracle():
             pairs = D.sample_pairs(n, min(500, n * (n - 1) // 2), case)
             cos, _ = D.pair_correlations(X, pairs)
             assert np.max(np.abs(cos - O.pair_cosines(X, pairs))) <= COS_ABS
+
+
+def test_large_k_global_counts():
+    """K above the 16384-cluster shared-histogram limit: counts and the
+    counting sort switch to global atomics; ~1 point per cluster also drives
+    thousands of empty-cluster reseeds per iteration."""
+    rng = np.random.default_rng(77)
+    X = rng.standard_normal((17_000, 3))
+    a = pcl.kmeans(X, 16_500, max_iters=2, seed=5)
+    labels, hist = O.kmeans(X, 16_500, max_iters=2, seed=5)
+    assert np.array_equal(a.labels, labels)
+    _close_hist(a.inertia_history, hist, X)
