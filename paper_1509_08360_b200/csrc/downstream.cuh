@@ -467,24 +467,29 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
             const double *cr = Ct + co * G.rs;
             double dot[2];
             if (T > 0) {
+                // lane-permuted slots: row slot i holds row i ^ mi, centroid slot q holds
+                // q ^ 2 b2, so the transpose-reduce below keeps fixed registers (no
+                // lane-dependent selects) and partners' halves line up slot for slot
                 double acc[4][4];
-                const double *xj = xr + j * G.tp, *cj = cr + j * G.tp;
-                // body: first step peeled (r[j] starts at the first product), then
-                // pairs of steps per 16-byte load, the odd last step peeled
+                const double *xs[4], *cs[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) xs[i] = xr + (i ^ mi) * G.rs + j * G.tp;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cs[q] = cr + (q ^ (2 * b2)) * G.rs + j * G.tp;
                 {
                     double2 xv[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xj + i * G.rs);
+                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xs[i]);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const double2 cv = *reinterpret_cast<const double2 *>(cj + q * G.rs);
+                        const double2 cv = *reinterpret_cast<const double2 *>(cs[q]);
 #pragma unroll
                         for (int i = 0; i < 4; ++i) acc[i][q] = __dmul_rn(xv[i].x, cv.x);
                     }
                     if (T > 1) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const double cy = cj[q * G.rs + 1];
+                            const double cy = cs[q][1];
 #pragma unroll
                             for (int i = 0; i < 4; ++i) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i].y, cy));
                         }
@@ -494,10 +499,10 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
                 for (; t + 1 < T; t += 2) {
                     double2 xv[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xj + i * G.rs + t);
+                    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const double2 *>(xs[i] + t);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const double2 cv = *reinterpret_cast<const double2 *>(cj + q * G.rs + t);
+                        const double2 cv = *reinterpret_cast<const double2 *>(cs[q] + t);
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xv[i].x, cv.x));
@@ -508,30 +513,24 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
                 if (t < T) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const double cx = cj[q * G.rs + t];
+                        const double cx = cs[q][t];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xj[i * G.rs + t], cx));
+                        for (int i = 0; i < 4; ++i) acc[i][q] = __dadd_rn(acc[i][q], __dmul_rn(xs[i][t], cx));
                     }
                 }
                 // transpose-reduce over the 8 residue lanes in numpy's tree order
-                // (xor 1, 2, 4 = (r0+r1), (r01+r23), (r0123+r4567)); each round keeps
-                // the half of the (row, centroid) pairs selected by one lane bit
+                // (xor 1, 2, 4 = (r0+r1), (r01+r23), (r0123+r4567)): keep slots 0..half-1,
+                // send the rest; the partner holds the same pairs in those slots
                 double r1[8], r2[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {  // pair (i, q) = (2 * bit + (e >> 2), e & 3)
-                    const double lo = acc[e >> 2][e & 3], hi = acc[2 + (e >> 2)][e & 3];
-                    r1[e] = __dadd_rn(b0 ? hi : lo, __shfl_xor_sync(0xffffffffu, b0 ? lo : hi, 1));
-                }
+                for (int e = 0; e < 8; ++e)  // slots (i, q) = (e >> 2, e & 3) kept, (2 + (e >> 2), e & 3) sent
+                    r1[e] = __dadd_rn(acc[e >> 2][e & 3], __shfl_xor_sync(0xffffffffu, acc[2 + (e >> 2)][e & 3], 1));
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {  // row bit 0
-                    const double lo = r1[e], hi = r1[4 + e];
-                    r2[e] = __dadd_rn(b1 ? hi : lo, __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2));
-                }
+                for (int e = 0; e < 4; ++e)  // row slot 0 kept, 1 sent
+                    r2[e] = __dadd_rn(r1[e], __shfl_xor_sync(0xffffffffu, r1[4 + e], 2));
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {  // centroid bit 1
-                    const double lo = r2[e], hi = r2[2 + e];
-                    dot[e] = __dadd_rn(b2 ? hi : lo, __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4));
-                }
+                for (int e = 0; e < 2; ++e)  // centroid slots 0, 1 kept, 2, 3 sent
+                    dot[e] = __dadd_rn(r2[e], __shfl_xor_sync(0xffffffffu, r2[2 + e], 4));
             } else {
                 dot[0] = dot[1] = -0.0;  // numpy: rows shorter than 8 sum from -0.0
             }
