@@ -83,14 +83,14 @@ static cudaError_t rec_event(csemb_plan *p, int i, cudaStream_t s) {
                         : cudaEventRecord(p->ev[i], s);
 }
 
-static void sched_free(Schedule *sc) {
+static void sched_free(csemb_ctx *c, Schedule *sc) {
     if (!sc) return;
-    cudaFree(sc->perm);
-    cudaFree(sc->cbeg);
-    cudaFree(sc->cend);
-    cudaFree(sc->hrows);
-    cudaFree(sc->hoff);
-    cudaFree(sc->corder);
+    dfree(c, sc->perm);
+    dfree(c, sc->cbeg);
+    dfree(c, sc->cend);
+    dfree(c, sc->hrows);
+    dfree(c, sc->hoff);
+    dfree(c, sc->corder);
     delete sc;
 }
 
@@ -384,41 +384,45 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
     sc->n_chunks = (int64_t)cbeg.size();
     cudaError_t e = cudaSuccess;
     if (bucket || sc->n_heavy > 0) {
-        e = cudaMalloc(&sc->perm, sizeof(int) * std::max<size_t>(light.size(), 1));
+        e = dmalloc(m->ctx, &sc->perm, sizeof(int) * std::max<size_t>(light.size(), 1));
         if (e == cudaSuccess && !light.empty())
-            e = cudaMemcpy(sc->perm, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice);
+            e = cudaMemcpyAsync(sc->perm, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice,
+                                m->ctx->stream);
     }
     if (e == cudaSuccess && sc->n_heavy > 0) {
-        e = cudaMalloc(&sc->cbeg, 8 * cbeg.size());
-        if (e == cudaSuccess) e = cudaMalloc(&sc->cend, 8 * cend.size());
-        if (e == cudaSuccess) e = cudaMalloc(&sc->hrows, 4 * hrows.size());
-        if (e == cudaSuccess) e = cudaMalloc(&sc->hoff, 4 * hoff.size());
-        if (e == cudaSuccess) e = cudaMemcpy(sc->cbeg, cbeg.data(), 8 * cbeg.size(), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(sc->cend, cend.data(), 8 * cend.size(), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(sc->hrows, hrows.data(), 4 * hrows.size(), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(sc->hoff, hoff.data(), 4 * hoff.size(), cudaMemcpyHostToDevice);
+        e = dmalloc(m->ctx, &sc->cbeg, 8 * cbeg.size());
+        if (e == cudaSuccess) e = dmalloc(m->ctx, &sc->cend, 8 * cend.size());
+        if (e == cudaSuccess) e = dmalloc(m->ctx, &sc->hrows, 4 * hrows.size());
+        if (e == cudaSuccess) e = dmalloc(m->ctx, &sc->hoff, 4 * hoff.size());
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sc->cbeg, cbeg.data(), 8 * cbeg.size(), cudaMemcpyHostToDevice, m->ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sc->cend, cend.data(), 8 * cend.size(), cudaMemcpyHostToDevice, m->ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sc->hrows, hrows.data(), 4 * hrows.size(), cudaMemcpyHostToDevice, m->ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(sc->hoff, hoff.data(), 4 * hoff.size(), cudaMemcpyHostToDevice, m->ctx->stream);
         // order the chunks by their first column (results do not depend on it)
         int *first = nullptr;
         std::vector<int> hfirst(cbeg.size());
-        if (e == cudaSuccess) e = cudaMalloc(&first, 4 * cbeg.size());
+        if (e == cudaSuccess) e = dmalloc(m->ctx, &first, 4 * cbeg.size());
         if (e == cudaSuccess) {
-            k_gather_cols<<<grid_for((int64_t)cbeg.size(), 256, m->ctx->sm_count), 256>>>(m->cols, sc->cbeg, first,
+            k_gather_cols<<<grid_for((int64_t)cbeg.size(), 256, m->ctx->sm_count), 256, 0, m->ctx->stream>>>(m->cols, sc->cbeg, first,
                                                                                          (int64_t)cbeg.size());
             e = cudaGetLastError();
         }
-        if (e == cudaSuccess) e = cudaMemcpy(hfirst.data(), first, 4 * cbeg.size(), cudaMemcpyDeviceToHost);
-        cudaFree(first);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hfirst.data(), first, 4 * cbeg.size(), cudaMemcpyDeviceToHost, m->ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(m->ctx->stream);
+        dfree(m->ctx, first);
         if (e == cudaSuccess) {
             std::vector<int> ord(cbeg.size());
             for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
             std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hfirst[a] < hfirst[b]; });
-            e = cudaMalloc(&sc->corder, 4 * ord.size());
-            if (e == cudaSuccess) e = cudaMemcpy(sc->corder, ord.data(), 4 * ord.size(), cudaMemcpyHostToDevice);
+            e = dmalloc(m->ctx, &sc->corder, 4 * ord.size());
+            if (e == cudaSuccess) e = cudaMemcpyAsync(sc->corder, ord.data(), 4 * ord.size(), cudaMemcpyHostToDevice, m->ctx->stream);
         }
     }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(m->ctx->stream);  // host vectors go out of scope
     if (e != cudaSuccess) {
         cudaGetLastError();
-        sched_free(sc);
+        sched_free(m->ctx, sc);
         return fail(e == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, "schedule: %s",
                     cudaGetErrorString(e));
     }
@@ -459,7 +463,20 @@ extern "C" int csemb_ctx_create(int device, csemb_ctx **out) {
     c->device = device;
     cudaError_t e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {  // this context's memory pool: keeps up to min(8 GiB, 10% of HBM) cached
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        e = cudaMemPoolCreate(&c->pool, &props);
+        size_t fr = 0, tot = 0;
+        if (e == cudaSuccess) e = cudaMemGetInfo(&fr, &tot);
+        uint64_t keep = std::min<uint64_t>((uint64_t)8 << 30, (uint64_t)tot / 10);
+        if (e == cudaSuccess) e = cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     if (e != cudaSuccess) {
+        if (c->pool) cudaMemPoolDestroy(c->pool);
+        if (c->stream) cudaStreamDestroy(c->stream);
         delete c;
         return fail(CSEMB_ERR_CUDA, "context setup: %s", cudaGetErrorString(e));
     }
@@ -471,21 +488,38 @@ extern "C" int csemb_ctx_destroy(csemb_ctx *c) {
     if (!c) return CSEMB_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    cudaFree(c->scratch);
+    dfree(c, c->scratch);
+    cudaStreamSynchronize(c->stream);
+    cudaMemPoolDestroy(c->pool);
     cudaStreamDestroy(c->stream);
     delete c;
     return CSEMB_OK;
+}
+
+cudaError_t dmalloc(csemb_ctx *c, void **p, size_t bytes) {
+    cudaError_t e = cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 1), c->pool, c->stream);
+    if (e == cudaErrorMemoryAllocation) {  // give the pool's cached blocks back and retry once
+        cudaGetLastError();
+        cudaStreamSynchronize(c->stream);
+        cudaMemPoolTrimTo(c->pool, 0);
+        e = cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 1), c->pool, c->stream);
+    }
+    return e;
+}
+
+void dfree(csemb_ctx *c, void *p) {
+    if (p) cudaFreeAsync(p, c->stream);
 }
 
 cudaError_t ctx_scratch(csemb_ctx *c, size_t bytes, void **out) {
     if (bytes > c->scratch_bytes) {
         cudaError_t e = cudaStreamSynchronize(c->stream);  // the old buffer may still be in use
         if (e != cudaSuccess) return e;
-        cudaFree(c->scratch);
+        dfree(c, c->scratch);
         c->scratch = nullptr;
         c->scratch_bytes = 0;
         const size_t grow = std::max(bytes, (size_t)1 << 20);
-        e = cudaMalloc(&c->scratch, grow);
+        e = dmalloc(c, &c->scratch, grow);
         if (e != cudaSuccess) return e;
         c->scratch_bytes = grow;
     }
@@ -513,10 +547,10 @@ extern "C" int csemb_ctx_sm_count(csemb_ctx *c, int *out) {
 // ---------------------------------------------------------------------------
 static void mat_free(csemb_mat *m) {
     if (!m) return;
-    for (Schedule *sc : m->schedules) sched_free(sc);
-    cudaFree(m->rowptr);
-    cudaFree(m->cols);
-    cudaFree(m->vals);
+    for (Schedule *sc : m->schedules) sched_free(m->ctx, sc);
+    dfree(m->ctx, m->rowptr);
+    dfree(m->ctx, m->cols);
+    dfree(m->ctx, m->vals);
     delete m;
 }
 
@@ -532,9 +566,9 @@ static int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, 
     m->n_cols = n_cols;
     m->nnz = nnz;
     m->dtype = dtype;
-    cudaError_t e = cudaMalloc(&m->rowptr, sizeof(int64_t) * (size_t)(n_rows + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&m->cols, sizeof(int) * (size_t)std::max<int64_t>(nnz, 1));
-    if (e == cudaSuccess) e = cudaMalloc(&m->vals, dsize(dtype) * (size_t)std::max<int64_t>(nnz, 1));
+    cudaError_t e = dmalloc(c, &m->rowptr, sizeof(int64_t) * (size_t)(n_rows + 1));
+    if (e == cudaSuccess) e = dmalloc(c, &m->cols, sizeof(int) * (size_t)std::max<int64_t>(nnz, 1));
+    if (e == cudaSuccess) e = dmalloc(c, &m->vals, dsize(dtype) * (size_t)std::max<int64_t>(nnz, 1));
     if (e != cudaSuccess) {
         cudaGetLastError();
         mat_free(m);
@@ -592,9 +626,9 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
     const int64_t CH = std::min<int64_t>(std::max<int64_t>(nnz, 1), (int64_t)1 << 25);
     void *st_cols = nullptr, *st_vals = nullptr;
     int *bad = nullptr;
-    if (e == cudaSuccess) e = cudaMalloc(&st_cols, 8 * (size_t)CH);
-    if (e == cudaSuccess) e = cudaMalloc(&st_vals, 8 * (size_t)CH);
-    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
+    if (e == cudaSuccess) e = dmalloc(c, &st_cols, 8 * (size_t)CH);
+    if (e == cudaSuccess) e = dmalloc(c, &st_vals, 8 * (size_t)CH);
+    if (e == cudaSuccess) e = dmalloc(c, &bad, sizeof(int));
     if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
     for (int64_t off = 0; e == cudaSuccess && off < nnz; off += CH) {
         const int64_t cnt = std::min(CH, nnz - off);
@@ -611,9 +645,9 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
     int hbad = 0;
     if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
-    cudaFree(st_cols);
-    cudaFree(st_vals);
-    cudaFree(bad);
+    dfree(c, st_cols);
+    dfree(c, st_vals);
+    dfree(c, bad);
     if (rc || e != cudaSuccess) {
         mat_free(m);
         if (rc) return rc;
@@ -645,7 +679,7 @@ extern "C" int csemb_matrix_upload_device(csemb_ctx *c, int64_t n_rows, int64_t 
     int *bad = nullptr;
     cudaError_t e = cudaMemcpyAsync(m->rowptr, row_offsets_dev, sizeof(int64_t) * (size_t)(n_rows + 1),
                                     cudaMemcpyDeviceToDevice, s);
-    if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
+    if (e == cudaSuccess) e = dmalloc(c, &bad, sizeof(int));
     if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), s);
     if (e == cudaSuccess && nnz > 0) rc = mat_fill_chunk(m, 0, nnz, col_indices_dev, idx_bytes, values_dev, bad);
     int hbad = 0;
@@ -654,7 +688,7 @@ extern "C" int csemb_matrix_upload_device(csemb_ctx *c, int64_t n_rows, int64_t 
     if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&ends[0], m->rowptr, 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&ends[1], m->rowptr + n_rows, 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
-    cudaFree(bad);
+    dfree(c, bad);
     if (rc || e != cudaSuccess) {
         mat_free(m);
         if (rc) return rc;
@@ -685,7 +719,10 @@ extern "C" int csemb_matrix_destroy(csemb_mat *m) {
     if (!m) return CSEMB_OK;
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     cudaSetDevice(m->ctx->device);
-    cudaStreamSynchronize(m->ctx->stream);
+    // other streams (caller code reading an output buffer) may still use this
+    // memory: wait for the device, as cudaFree would, before the blocks return
+    // to the stream-ordered pool
+    cudaDeviceSynchronize();
     mat_free(m);
     return CSEMB_OK;
 }
@@ -725,11 +762,11 @@ extern "C" int csemb_matrix_download_values(csemb_mat *m, double *values_out) {
         CK(cudaMemcpyAsync(values_out, m->vals, 8 * (size_t)m->nnz, cudaMemcpyDeviceToHost, s));
     } else {
         double *tmp = nullptr;
-        CK(cudaMalloc(&tmp, 8 * (size_t)m->nnz));
+        CK(dmalloc(m->ctx, &tmp, 8 * (size_t)m->nnz));
         k_vals_to_f64<float><<<grid_for(m->nnz, 256, m->ctx->sm_count), 256, 0, s>>>((const float *)m->vals, tmp, m->nnz);
         cudaError_t e = cudaMemcpyAsync(values_out, tmp, 8 * (size_t)m->nnz, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(tmp);
+        dfree(m->ctx, tmp);
         CK(e);
     }
     CK(cudaStreamSynchronize(s));
@@ -741,12 +778,12 @@ extern "C" int csemb_matrix_download_values(csemb_mat *m, double *values_out) {
 // ---------------------------------------------------------------------------
 static void plan_free(csemb_plan *p) {
     if (!p) return;
-    cudaFree(p->y[0]);
-    cudaFree(p->y[1]);
-    cudaFree(p->E);
-    cudaFree(p->staging);
-    cudaFree(p->peaks);
-    cudaFree(p->partials);
+    dfree(p->m->ctx, p->y[0]);
+    dfree(p->m->ctx, p->y[1]);
+    dfree(p->m->ctx, p->E);
+    dfree(p->m->ctx, p->staging);
+    dfree(p->m->ctx, p->peaks);
+    dfree(p->m->ctx, p->partials);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
@@ -770,9 +807,9 @@ extern "C" int csemb_plan_create(csemb_mat *m, int64_t d, csemb_plan **out) {
         return fail(CSEMB_ERR_UNSUPPORTED, "d too large");
     }
     const size_t bytes = dsize(m->dtype) * (size_t)std::max<int64_t>(m->n_rows, 1) * (size_t)p->ld;
-    cudaError_t e = cudaMalloc(&p->y[0], bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&p->y[1], bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&p->E, bytes);
+    cudaError_t e = dmalloc(p->m->ctx, &p->y[0], bytes);
+    if (e == cudaSuccess) e = dmalloc(p->m->ctx, &p->y[1], bytes);
+    if (e == cudaSuccess) e = dmalloc(p->m->ctx, &p->E, bytes);
     for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&p->ev[i]);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -815,7 +852,10 @@ extern "C" int csemb_plan_destroy(csemb_plan *p) {
     if (!p) return CSEMB_OK;
     std::lock_guard<std::mutex> lk(p->m->ctx->mu);
     cudaSetDevice(p->m->ctx->device);
-    cudaStreamSynchronize(p->m->ctx->stream);
+    // other streams (caller code reading an output buffer) may still use this
+    // memory: wait for the device, as cudaFree would, before the blocks return
+    // to the stream-ordered pool
+    cudaDeviceSynchronize();
     plan_free(p);
     return CSEMB_OK;
 }
@@ -834,10 +874,10 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
     const int64_t n_chunks = (d_global + 31) / 32;
     const size_t need = (size_t)n_stages * (size_t)std::max(order, 0) * (size_t)n_chunks;
     if (need > p->peaks_cap) {
-        cudaFree(p->peaks);
+        dfree(c, p->peaks);
         p->peaks = nullptr;
         p->peaks_cap = 0;
-        CK(cudaMalloc(&p->peaks, sizeof(unsigned long long) * need));
+        CK(dmalloc(c, &p->peaks, sizeof(unsigned long long) * need));
         p->peaks_cap = need;
     }
     if (need) CK(cudaMemsetAsync(p->peaks, 0, sizeof(unsigned long long) * need, s));
@@ -858,10 +898,10 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
         if (rc) return rc;
         const size_t pbytes = (size_t)sc->n_chunks * (size_t)ld * sizeof(T);
         if (pbytes > p->partials_bytes) {
-            cudaFree(p->partials);
+            dfree(c, p->partials);
             p->partials = nullptr;
             p->partials_bytes = 0;
-            CK(cudaMalloc(&p->partials, pbytes));
+            CK(dmalloc(c, &p->partials, pbytes));
             p->partials_bytes = pbytes;
         }
     }
@@ -1017,10 +1057,10 @@ static int plan_download_locked(csemb_plan *p, void *out_host, int out_dtype) {
         // convert into the staging buffer (big enough for n x d f64), then copy
         const size_t need = 8 * (size_t)n * (size_t)d;
         if (p->staging_bytes < need) {
-            cudaFree(p->staging);
+            dfree(p->m->ctx, p->staging);
             p->staging = nullptr;
             p->staging_bytes = 0;
-            CK(cudaMalloc(&p->staging, need));
+            CK(dmalloc(p->m->ctx, &p->staging, need));
             p->staging_bytes = need;
         }
         const int g = grid_for(n * (int64_t)d, 256, m->ctx->sm_count, 16);
@@ -1141,10 +1181,10 @@ extern "C" int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int or
         if (!block_host) return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
         const size_t need = 8 * (size_t)n * (size_t)p->d;
         if (p->staging_bytes < need) {
-            cudaFree(p->staging);
+            dfree(p->m->ctx, p->staging);
             p->staging = nullptr;
             p->staging_bytes = 0;
-            CK(cudaMalloc(&p->staging, need));
+            CK(dmalloc(p->m->ctx, &p->staging, need));
             p->staging_bytes = need;
         }
         CK(cudaMemcpyAsync(p->staging, block_host, need, cudaMemcpyHostToDevice, m->ctx->stream));
@@ -1195,10 +1235,10 @@ static int plan_begin_t(csemb_plan *p, const double *block_dev, int omega_kind, 
     const int64_t n_chunks = (p->d_global + 31) / 32;
     const size_t need = (size_t)std::max(order, 0) * (size_t)n_chunks;
     if (need > p->peaks_cap) {
-        cudaFree(p->peaks);
+        dfree(c, p->peaks);
         p->peaks = nullptr;
         p->peaks_cap = 0;
-        CK(cudaMalloc(&p->peaks, sizeof(unsigned long long) * need));
+        CK(dmalloc(c, &p->peaks, sizeof(unsigned long long) * need));
         p->peaks_cap = need;
     }
     if (need) CK(cudaMemsetAsync(p->peaks, 0, sizeof(unsigned long long) * need, s));
@@ -1255,10 +1295,10 @@ static int plan_step_t(csemb_plan *p, int r) {
     if (rc) return rc;
     const size_t pbytes = (size_t)sc->n_chunks * (size_t)p->ld * sizeof(T);
     if (pbytes > p->partials_bytes) {
-        cudaFree(p->partials);
+        dfree(c, p->partials);
         p->partials = nullptr;
         p->partials_bytes = 0;
-        CK(cudaMalloc(&p->partials, pbytes));
+        CK(dmalloc(c, &p->partials, pbytes));
         p->partials_bytes = pbytes;
     }
     StepParams P;
@@ -1335,14 +1375,14 @@ extern "C" int csemb_sample_projection(csemb_ctx *c, int64_t n, int64_t d_global
     CK(cudaSetDevice(c->device));
     if (w == 0) return CSEMB_OK;
     double *buf = nullptr;
-    CK(cudaMalloc(&buf, 8 * (size_t)n * (size_t)w));
+    CK(dmalloc(c, &buf, 8 * (size_t)n * (size_t)w));
     k_omega_dense<<<grid_for(n * w, 256, c->sm_count, 16), 256, 0, c->stream>>>(
         buf, n, w, kind, seed, col0, d_global, 1.0 / std::sqrt((double)d_global));
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(out_host, buf, 8 * (size_t)n * (size_t)w, cudaMemcpyDeviceToHost, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    cudaFree(buf);
+    dfree(c, buf);
     CK(e);
     return CSEMB_OK;
 }
@@ -1365,13 +1405,13 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     double *stage = nullptr, *partial = nullptr, *rq = nullptr, *inv = nullptr;
     const size_t blk = sizeof(T) * (size_t)n * ld;
     std::vector<double> hrq;
-    cudaError_t e = cudaMalloc(&V, blk);
-    if (e == cudaSuccess) e = cudaMalloc(&Wm, blk);
-    if (e == cudaSuccess) e = cudaMalloc(&partial, sizeof(double) * 2 * (size_t)gy * k);
-    if (e == cudaSuccess) e = cudaMalloc(&rq, sizeof(double) * (size_t)iters * k);
-    if (e == cudaSuccess) e = cudaMalloc(&inv, sizeof(double) * (size_t)k);
+    cudaError_t e = dmalloc(c, &V, blk);
+    if (e == cudaSuccess) e = dmalloc(c, &Wm, blk);
+    if (e == cudaSuccess) e = dmalloc(c, &partial, sizeof(double) * 2 * (size_t)gy * k);
+    if (e == cudaSuccess) e = dmalloc(c, &rq, sizeof(double) * (size_t)iters * k);
+    if (e == cudaSuccess) e = dmalloc(c, &inv, sizeof(double) * (size_t)k);
     if (e == cudaSuccess && v0_host) {
-        e = cudaMalloc(&stage, sizeof(double) * (size_t)n * k);
+        e = dmalloc(c, &stage, sizeof(double) * (size_t)n * k);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(stage, v0_host, sizeof(double) * (size_t)n * k, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) {
@@ -1395,10 +1435,10 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     if (e == cudaSuccess) {
         const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), 4096, -1, &sc);
         if (rc) {
-            cudaFree(V); cudaFree(Wm); cudaFree(stage); cudaFree(partial); cudaFree(rq); cudaFree(inv);
+            dfree(c, V); dfree(c, Wm); dfree(c, stage); dfree(c, partial); dfree(c, rq); dfree(c, inv);
             return rc;
         }
-        if (sc->n_chunks) e = cudaMalloc(&partials, (size_t)sc->n_chunks * (size_t)ld * sizeof(T));
+        if (sc->n_chunks) e = dmalloc(c, &partials, (size_t)sc->n_chunks * (size_t)ld * sizeof(T));
     }
     for (int it = 0; it < iters && e == cudaSuccess; ++it) {
         StepParams P;
@@ -1425,13 +1465,13 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
         e = cudaMemcpyAsync(hrq.data(), rq, sizeof(double) * hrq.size(), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     }
-    cudaFree(V);
-    cudaFree(Wm);
-    cudaFree(stage);
-    cudaFree(partials);
-    cudaFree(partial);
-    cudaFree(rq);
-    cudaFree(inv);
+    dfree(c, V);
+    dfree(c, Wm);
+    dfree(c, stage);
+    dfree(c, partials);
+    dfree(c, partial);
+    dfree(c, rq);
+    dfree(c, inv);
     CK(e);
     double best = 0.0;
     for (double v : hrq) best = std::max(best, std::fabs(v));

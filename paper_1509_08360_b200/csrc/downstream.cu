@@ -57,7 +57,7 @@ static void km_free(csemb_kmeans *k) {
     for (void *p : {(void *)k->X, (void *)k->xx, (void *)k->C, (void *)k->cc, (void *)k->closest, (void *)k->mind,
                     (void *)k->lab, (void *)k->lab_new, (void *)k->counts, (void *)k->part, (void *)k->part_i,
                     (void *)k->scal, (void *)k->pick, (void *)k->seg_off, (void *)k->order, (void *)k->start})
-        cudaFree(p);
+        dfree(k->ctx, p);
     delete k;
 }
 
@@ -87,7 +87,7 @@ extern "C" int csemb_pair_cosines(csemb_ctx *c, const void *E, int dtype, int on
     double *dout = (double *)(dp + 2 * n_pairs);
     uint8_t *dz = (uint8_t *)(dout + n_pairs);
     if (e == cudaSuccess && !on_device) {  // host block: one upload, row stride d
-        e = cudaMalloc(&dE, es * n * d);
+        e = dmalloc(c, &dE, es * n * d);
         if (e == cudaSuccess) e = cudaMemcpy2DAsync(dE, es * d, E, es * ld, es * d, n, cudaMemcpyHostToDevice, s);
     }
     const void *src = on_device ? E : dE;
@@ -104,7 +104,7 @@ extern "C" int csemb_pair_cosines(csemb_ctx *c, const void *E, int dtype, int on
     if (e == cudaSuccess) e = cudaMemcpyAsync(cos_out, dout, 8 * n_pairs, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && zero_out) e = cudaMemcpyAsync(zero_out, dz, n_pairs, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(dE);
+    dfree(c, dE);
     CK(e);
     return CSEMB_OK;
 }
@@ -143,7 +143,7 @@ extern "C" int csemb_kmeans_create(csemb_ctx *c, const void *X, int dtype, int o
     k->nseg = (n + k->seg - 1) / k->seg;
     cudaError_t e = cudaSuccess;
     auto A = [&](void **p, size_t bytes) {
-        if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(bytes, 8));
+        if (e == cudaSuccess) e = dmalloc(c, p, std::max<size_t>(bytes, 8));
     };
     A((void **)&k->X, 8 * n * k->ld);
     A((void **)&k->xx, 8 * n);
@@ -191,7 +191,10 @@ extern "C" int csemb_kmeans_destroy(csemb_kmeans *k) {
     if (!k) return CSEMB_OK;
     std::lock_guard<std::mutex> lk(k->ctx->mu);
     cudaSetDevice(k->ctx->device);
-    cudaStreamSynchronize(k->ctx->stream);
+    // other streams (caller code reading an output buffer) may still use this
+    // memory: wait for the device, as cudaFree would, before the blocks return
+    // to the stream-ordered pool
+    cudaDeviceSynchronize();
     km_free(k);
     return CSEMB_OK;
 }
@@ -399,8 +402,8 @@ extern "C" int csemb_modularity_counts(csemb_mat *m, const int32_t *labels, int 
     cudaStream_t s = c->stream;
     int *dl = nullptr;
     unsigned long long *cnt = nullptr;
-    cudaError_t e = cudaMalloc(&cnt, 16 * (size_t)k + 8);  // [k] intra2, [k] degsum, bad-label count
-    if (e == cudaSuccess && !on_device) e = cudaMalloc(&dl, 4 * std::max<int64_t>(n, 1));
+    cudaError_t e = dmalloc(c, &cnt, 16 * (size_t)k + 8);  // [k] intra2, [k] degsum, bad-label count
+    if (e == cudaSuccess && !on_device) e = dmalloc(c, &dl, 4 * std::max<int64_t>(n, 1));
     if (e == cudaSuccess && !on_device && n) e = cudaMemcpyAsync(dl, labels, 4 * n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 16 * (size_t)k + 8, s);
     if (e == cudaSuccess && n) {
@@ -420,8 +423,8 @@ extern "C" int csemb_modularity_counts(csemb_mat *m, const int32_t *labels, int 
     std::vector<unsigned long long> h(2 * (size_t)k + 1);
     if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), cnt, 16 * (size_t)k + 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    cudaFree(dl);
-    cudaFree(cnt);
+    dfree(c, dl);
+    dfree(c, cnt);
     CK(e);
     if (h[2 * k]) return fail(CSEMB_ERR_INVALID, "%llu labels outside [0, %lld)", h[2 * k], (long long)k);
     for (int64_t q = 0; q < k; ++q) {

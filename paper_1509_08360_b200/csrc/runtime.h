@@ -38,7 +38,19 @@ struct csemb_ctx {
     std::mutex mu;
     void *scratch = nullptr;  // grow-only device scratch for per-call temporaries
     size_t scratch_bytes = 0;
+    cudaMemPool_t pool = nullptr;  // stream-ordered allocations of this context (dmalloc/dfree)
 };
+
+// Device memory of a context: stream-ordered allocations from the context's pool
+// on its stream.  Freed blocks stay in the pool (up to its release threshold)
+// and are reused without cudaMalloc/cudaFree round trips; an allocation that
+// fails trims the pool and retries once.
+CSEMB_INTERNAL cudaError_t dmalloc(csemb_ctx *c, void **p, size_t bytes);
+CSEMB_INTERNAL void dfree(csemb_ctx *c, void *p);
+template <typename T>
+static inline cudaError_t dmalloc(csemb_ctx *c, T **p, size_t bytes) {
+    return dmalloc(c, reinterpret_cast<void **>(p), bytes);
+}
 
 // the context's scratch buffer with at least `bytes` (call with c->mu held;
 // valid until the next call that grows it)
