@@ -14,7 +14,9 @@ value  = T*d*L / device time per step (CUDA events, inputs resident in HBM;
          the working set -- 2 x 640 MB Q buffers + 640 MB E + 240 MB CSR in
          f64 -- is far larger than the 126 MB L2, so no flush is needed).
 e2e    = same metric through the reference-facing C ABI call with HOST
-         buffers: CSR upload + projection block H2D + E D2H every step.
+         buffers, the reference's default entry (fast_embed_cascaded with
+         omega=None): CSR upload (H2D) every step, Omega generated on the
+         device bit-identical to the reference's sample_projection, E D2H.
 roofline: K1's algorithmic bytes per launch, B = T*(4+8) + 5*n*d*8 (f64) /
          T*(4+4) + 5*n*d*4 (f32), over K1's average launch time (CUDA events
          on the library stream), against MEASURED_PEAKS.json hbm_gbs.
@@ -280,7 +282,10 @@ def _gather_columns(plan, dm, n, d, world, rank, local_rank, dtype):
 
 
 def run_e2e(args, S, coeffs, units, device):
-    """Reference-facing call with host buffers: upload CSR + block, run, download E."""
+    """Reference-facing call with host buffers, the reference's default entry
+    fast_embed_cascaded(S, f, cfg) (omega=None: Omega = sample_projection(n, d,
+    seed), engine.py:319-320): upload the CSR, generate Omega on the device with
+    the reference's SplitMix64 hash (bit-identical), run, download E."""
     import torch
 
     import paper_1509_08360_b200 as pb
@@ -289,13 +294,12 @@ def run_e2e(args, S, coeffs, units, device):
     n, d = S.n_rows, args.d
     pin = lambda a: torch.from_numpy(np.array(a)).pin_memory()  # noqa: E731
     ro, ci, va = pin(S.row_offsets), pin(S.col_indices), pin(S.values)
-    block = pin(pb.sample_projection(n, d, 7))
     out = torch.empty((n, d), dtype=torch.float64).pin_memory()
     ctx = _lib.context(device)
     lib = ctx.lib
     import ctypes as C
 
-    h2d = ro.numel() * 8 + ci.numel() * 8 + va.numel() * 8 + block.numel() * 8
+    h2d = ro.numel() * 8 + ci.numel() * 8 + va.numel() * 8
     d2h = out.numel() * 8
     c = np.ascontiguousarray(coeffs)
 
@@ -306,8 +310,8 @@ def run_e2e(args, S, coeffs, units, device):
                                            C.byref(h)))
         dm = pb.DeviceMatrix(None, "float64", device, _handle=h)
         p = dm.plan(d)
-        rc = lib.csemb_apply_expansion(p.handle, _lib.ptr(c), len(c) - 1, 1, C.c_void_p(block.data_ptr()),
-                                       _lib.OMEGA_GIVEN, 0, 0, d, 1, C.c_void_p(out.data_ptr()), None, None, None)
+        rc = lib.csemb_apply_expansion(p.handle, _lib.ptr(c), len(c) - 1, 1, None, _lib.OMEGA_SPLITMIX, 7, 0, d,
+                                       1, C.c_void_p(out.data_ptr()), None, None, None)
         _lib.check(rc)
         dm.close()
 
