@@ -43,6 +43,11 @@ template <> struct Vec<float> {
 __device__ __forceinline__ double2 vzero(double2) { return make_double2(0.0, 0.0); }
 __device__ __forceinline__ float4 vzero(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
+#ifndef K1_GATHER_PF
+#define K1_GATHER_PF 0  // 1: L2 prefetch of the next batch's gathered rows (B steps ahead);
+                        // measured +19% (f64) / +33% (f32) K1 time on config 2: the extra
+                        // requests compete with the gathers for L2 bandwidth
+#endif
 #ifndef K1_PREFETCH
 #define K1_PREFETCH 1  // L2 prefetch of the epilogue's streamed rows at the start of each row set (fp64)
 #endif
@@ -298,6 +303,9 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     bool valid[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) valid[k] = (gl + k * G) < P.nvt;
+#if K1_GATHER_PF
+    const int pf_lines = (P.nvt * 16 + 127) / 128 + 1;  // 128-byte lines a row tile touches (+1: alignment)
+#endif
     unsigned long long pk[PEAK == PEAK_EXACT ? VPL : 1];
 #pragma unroll
     for (int k = 0; k < (PEAK == PEAK_EXACT ? VPL : 1); ++k) pk[k] = 0ull;
@@ -443,6 +451,16 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             // batch or row-set epilogue starts with an empty pipeline) and consumes t
 #pragma unroll
             for (int t = 0; t < B; ++t) {
+#if K1_GATHER_PF
+                // L2 prefetch of entry t of the NEXT batch (B steps ahead, no registers):
+                // lanes gl < pf_lines each request one 128-byte line of that row, so the
+                // register gather D steps ahead finds it in L2
+                if constexpr (STAGED == 0) {
+                    const int jn = __shfl_sync(0xFFFFFFFFu, nj, t, G);
+                    if (gl < pf_lines && t < ncnt)
+                        prefetch_l2(reinterpret_cast<const char *>(ycur - gl + (int64_t)jn * P.ldv) + gl * 128);
+                }
+#endif
                 const int e = t + D - 1;
                 const int j = (e < B) ? __shfl_sync(0xFFFFFFFFu, myj, e % B, G)
                                       : __shfl_sync(0xFFFFFFFFu, nj, e % B, G);
