@@ -370,10 +370,13 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     }
     auto issue = [&](int slot, int j, bool ok) {
         if constexpr (STAGED == 2) {
+            // no copy at all for padding entries / unused vectors: a zero-fill copy
+            // (src_bytes 0) still fetched the source line and doubled L2->SM bytes
             const VT *x = ycur + (int64_t)j * P.ldv;
             VT *dst = lring + (size_t)slot * blockDim.x * VPL;
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) cp_async16(dst + k, x + k * G, (valid[k] && ok) ? 16 : 0);
+            for (int k = 0; k < VPL; ++k)
+                if (valid[k] && ok) cp_async16(dst + k, x + k * G, 16);
             cp_async_commit();
         } else if constexpr (STAGED == 1) {
             if (gl == 0) {
@@ -471,9 +474,9 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 if constexpr (STAGED == 2) {
                     cp_async_wait<D - 1>();  // entry t has landed (this lane's own copies)
                     const VT *src = lring + (size_t)(t % D) * blockDim.x * VPL;
-                    // padding steps were zero-filled and a == 0: acc + (+0) == acc exactly
+                    const bool ok = t < cnt;  // padding steps were never copied: skip them
 #pragma unroll
-                    for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, src[k]);
+                    for (int k = 0; k < VPL; ++k) acc[k] = vsel(ok, vmadd(acc[k], a, src[k]), acc[k]);
                 } else if constexpr (STAGED == 1) {
                     const int slot = t % D;
                     const unsigned par = (phase >> slot) & 1u;
