@@ -168,6 +168,8 @@ def _run_kmeans(km: DeviceKMeans, K: int, max_iters: int, seed: int) -> ClusterA
         if total <= 0.0:
             pick = int(rng.integers(n))
         else:
+            if not np.isfinite(total):  # rng.choice rejects such weights before drawing
+                raise ValueError("Probabilities contain NaN")
             pick = km.pick(float(rng.random()))  # == rng.choice(n, p=closest / total)
         total = km.seed(k, pick)
     history: list[float] = []

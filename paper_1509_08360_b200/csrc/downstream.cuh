@@ -377,8 +377,14 @@ __device__ __forceinline__ void ca_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void ca_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// np.argmin order: NaN is smallest (the first NaN wins), then value, then index
+__device__ __forceinline__ bool np_before(double v, int k, double bv, int bk) {
+    const bool vn = isnan(v), bn = isnan(bv);
+    if (vn | bn) return vn && (!bn || k < bk);
+    return v < bv || (v == bv && k < bk);
+}
 __device__ __forceinline__ void lexmin(double &bd, int &bk, double od, int ok) {
-    if (od < bd || (od == bd && ok < bk)) bd = od, bk = ok;
+    if (np_before(od, ok, bd, bk)) bd = od, bk = ok;
 }
 
 // residue-major geometry of one row: body elements c < body at [c % 8][c / 8]
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(KA_THREADS, 1) k_km_assign(
                 if (k < K) {
                     double v = __dsub_rn(__dadd_rn(xim, cc[k]), __dadd_rn(dot[e], dot[e]));
                     v = v < 0.0 ? 0.0 : v;  // np.maximum(v, 0.0): keeps NaN and -0.0
-                    if (v < bd) bd = v, bk = k;  // ascending k: first minimum
+                    if (v < bd || (isnan(v) && !isnan(bd))) bd = v, bk = k;  // ascending k: np.argmin
                 }
             }
         }

@@ -375,3 +375,22 @@ def test_large_k_global_counts():
     labels, hist = O.kmeans(X, 16_500, max_iters=2, seed=5)
     assert np.array_equal(a.labels, labels)
     _close_hist(a.inertia_history, hist, X)
+
+
+def test_nan_and_overflow_rows_follow_the_reference():
+    """Non-finite rows: the ++ seeding raises numpy's `Probabilities contain NaN`
+    (rng.choice) like the reference; with K=1 (no weighted pick) NaN flows
+    through Lloyd as in numpy (argmin treats NaN as the minimum)."""
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((50, 4))
+    X[7] = np.nan
+    with pytest.raises(ValueError, match="Probabilities contain NaN"):
+        pcl.kmeans(X, 3, seed=1)
+    Y = rng.standard_normal((50, 4))
+    Y[7, 0] = 1e200  # |x|^2 overflows to inf
+    with pytest.raises(ValueError, match="Probabilities contain NaN"):
+        pcl.kmeans(Y, 3, seed=1)
+    a = pcl.kmeans(X, 1, seed=1)
+    labels, hist = O.kmeans(X, 1, seed=1)
+    assert np.array_equal(a.labels, labels)
+    assert len(a.inertia_history) == len(hist) and all(np.isnan(a.inertia_history)) == all(np.isnan(hist))
