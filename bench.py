@@ -219,6 +219,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     res64, dm64, plan64 = measure("f64")
     log(f"[bench] f64: {res64['ms_per_step']:.2f} ms/step, K1 {res64['k1_ms']:.3f} ms, "
         f"{res64['roofline']['achieved']:.0f} GB/s ({res64['roofline']['frac']:.3f})")
+    down = None
+    if world == 1 and not args.skip_downstream:
+        down = run_downstream(dm64, plan64, n)
+        log(f"[bench] downstream: k-means K={down['K']} assign {down['assign_ms']:.3f} ms "
+            f"({down['assign_roofline']['frac']:.2f} of fp64), update {down['update_ms']:.3f} ms, "
+            f"pair cosines 1e5 {down['pair_cos_ms']:.3f} ms")
     res32 = None
     if not args.skip_fp32:
         dm64.close()
@@ -255,6 +261,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": cpu,
             "k1_ms": res64["k1_ms"],
         }
+        if down is not None:
+            line["downstream"] = down
         if res32 is not None:
             line["fp32"] = {"value": res32["value"], "ms_per_step": res32["ms_per_step"], "k1_ms": res32["k1_ms"],
                             "roofline": res32["roofline"], "clocks": res32["clocks"]}
@@ -279,6 +287,68 @@ def _gather_columns(plan, dm, n, d, world, rank, local_rank, dtype):
     _lib.check(dm.lib.csemb_rownorm(dm.ctx.handle, E.data_ptr(), n, d, d, _lib.F64 if dtype == "f64" else _lib.F32))
     dm.ctx.sync()  # E is torch-owned: finish the library-stream kernel before torch may recycle it
     return E
+
+
+def _fp64_peak():
+    """Measured FP64 DMUL+DADD ceiling (tools/fp64peak.cu, profiles/r1_fp64peak.txt)."""
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r1_fp64peak.txt")):
+            if line.startswith("dmul+dadd"):
+                return float(line.split()[1]), "measured (tools/fp64peak.cu, profiles/r1_fp64peak.txt)"
+    except (OSError, ValueError, IndexError):
+        pass
+    return None, None
+
+
+def run_downstream(dm, plan, n, K=100, iters=8):
+    """SURVEY 8(f) rank 4 on the headline embedding (still in HBM): k-means
+    (the reference's seeding + Lloyd steps, cluster.py:43-100), modularity
+    counts and 1e5 sampled-pair cosines, all on the device.  Wall time per
+    call (each call ends with its small device->host read)."""
+    from paper_1509_08360_b200 import cluster as pcl
+    from paper_1509_08360_b200 import distortion as D
+
+    rows = pcl.plan_rows(plan)
+    dm.ctx.sync()
+    km = pcl.DeviceKMeans(rows, K)
+    rng = np.random.default_rng(0x6B6D6531)
+    total = km.seed(0, int(rng.integers(n)))
+    for k in range(1, K):
+        total = km.seed(k, int(rng.integers(n)) if total <= 0.0 else km.pick(float(rng.random())))
+    a_ms, u_ms = [], []
+    for _ in range(iters):
+        t = time.perf_counter()
+        _, changed, counts = km.assign()
+        a_ms.append(1e3 * (time.perf_counter() - t))
+        if (counts == 0).any():
+            for c in np.flatnonzero(counts == 0):
+                km.reseed(int(c))
+            km.commit(False)
+            continue
+        t = time.perf_counter()
+        km.commit(True)
+        dm.ctx.sync()
+        u_ms.append(1e3 * (time.perf_counter() - t))
+    t = time.perf_counter()
+    k = int(km.labels().max()) + 1
+    intra, degsum = pcl.modularity_counts(dm, km.labels_device(), k)
+    mod_ms = 1e3 * (time.perf_counter() - t)
+    pairs = D.sample_pairs(n, 100_000, 1)
+    D.pair_correlations(rows, pairs[:1000])
+    t = time.perf_counter()
+    D.pair_correlations(rows, pairs)
+    pc_ms = 1e3 * (time.perf_counter() - t)
+    km.close()
+    d = plan.d
+    a = statistics.median(a_ms)
+    tflops = 2.0 * n * K * d / (a * 1e-3) / 1e12
+    peak, src = _fp64_peak()
+    return {"K": K, "lloyd_iters": iters, "assign_ms": a, "update_ms": statistics.median(u_ms) if u_ms else None,
+            "modularity_counts_ms": mod_ms, "pair_cos_ms": pc_ms, "pairs": len(pairs),
+            "modularity_Q": float(np.sum(intra / (dm.nnz // 2) - (degsum / (2.0 * (dm.nnz // 2))) ** 2)),
+            "assign_roofline": {"bound": "fp64", "achieved": round(tflops, 3), "peak": peak, "unit": "TFLOP/s",
+                                "frac": round(tflops / peak, 3) if peak else None, "peak_source": src,
+                                "flops_per_assign": 2.0 * n * K * d}}
 
 
 def run_e2e(args, S, coeffs, units, device):
@@ -413,6 +483,7 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
     ap.add_argument("--skip-fp32", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-downstream", action="store_true", help="omit the k-means / modularity / cosine object")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
