@@ -713,3 +713,41 @@ def test_graph_replay_bit_exact(config1):
     with pytest.raises(ValueError):
         plan.set_option(pb._lib.OPT_GRAPH, 2)
     dm.close()
+
+
+def test_out_of_memory_is_reported_and_context_survives(config1):
+    """An impossible allocation surfaces as MemoryError (CSEMB_ERR_NOMEM after
+    the pool is trimmed and the allocation retried); the context stays usable."""
+    z, meta = config1
+    dm = pb.DeviceMatrix(sparse_from(z), "float64")
+    with pytest.raises(MemoryError):
+        dm.plan(1_000_000_000)  # 3 x 2000 x 1e9 doubles
+    plan = dm.plan(40)
+    plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+    assert sha(plan.download()) == meta["E_sha256"]
+    dm.close()
+
+
+def test_repeated_create_destroy_does_not_grow_memory(config1):
+    """Matrices and plans come from the context's stream-ordered pool: many
+    create / run / destroy cycles reuse blocks instead of growing usage."""
+    import torch
+
+    z, meta = config1
+    S = sparse_from(z)
+
+    def cycle():
+        dm = pb.DeviceMatrix(S, "float64")
+        out = dm.plan(40).apply(z["coeffs"], 1, None, omega_kind=pb._lib.OMEGA_SPLITMIX)
+        dm.close()
+        return out
+
+    first = cycle()
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(25):
+        assert np.array_equal(cycle(), first)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20, (free0, free1)
+    assert sha(first) == meta["E_sha256"]
