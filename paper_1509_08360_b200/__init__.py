@@ -42,7 +42,14 @@ from .cluster import (
     modularity,
     plan_rows,
 )
-from .distortion import DistortionReport, distortion_percentiles, pair_correlations, sample_pairs
+from .distortion import (
+    DistortionReport,
+    distance_bound_audit,
+    distortion_percentiles,
+    exact_embedding,
+    pair_correlations,
+    sample_pairs,
+)
 from .errors import CsembError, CudaUnavailableError, DivergenceError, InputFormatError
 from .functions import (
     SpectralFunction,
@@ -82,5 +89,5 @@ __all__ = [
     # downstream consumers (cluster.py, oracle.py:88-186)
     "ClusterAssignment", "ClusterExperiment", "DeviceKMeans", "DeviceRows", "DistortionReport",
     "ModularityScore", "cluster_experiment", "distortion_percentiles", "kmeans", "modularity",
-    "pair_correlations", "plan_rows", "sample_pairs",
+    "pair_correlations", "plan_rows", "sample_pairs", "distance_bound_audit", "exact_embedding",
 ]

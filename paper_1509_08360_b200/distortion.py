@@ -26,8 +26,9 @@ import numpy as np
 
 from . import _lib
 from .cluster import DeviceRows
-from .engine import EmbeddingMatrix
+from .engine import EmbeddingMatrix, apply_expansion, fold_seed, sample_projection
 from .errors import OracleCapError, OracleError
+from .legendre import expansion_eval, legendre_coefficients
 from .sparse import SparseMatrix
 
 ORACLE_CAP = 3000          # oracle.py:22
@@ -75,12 +76,7 @@ class ExactEmbedding:
         return self.embedding.shape[0]
 
 
-def exact_embedding(S, f, cap: int = ORACLE_CAP, *, device: int = 0) -> ExactEmbedding:
-    """Exact embedding by a full dense symmetric eigendecomposition on the GPU
-    (oracle.py:46-71 semantics: square and symmetric to 1e-10, at most `cap`
-    rows, eigen-residual <= 1e-8, weights f(lambda), zero weights dropped)."""
-    import torch
-
+def _dense_symmetric(S, cap: int) -> np.ndarray:
     a = S.to_dense() if isinstance(S, SparseMatrix) else np.asarray(S, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError("expected a square matrix")
@@ -88,17 +84,73 @@ def exact_embedding(S, f, cap: int = ORACLE_CAP, *, device: int = 0) -> ExactEmb
         raise OracleCapError(f"matrix of size {a.shape[0]} exceeds the dense-oracle cap {cap}")
     if np.max(np.abs(a - a.T), initial=0.0) > 1e-10:
         raise ValueError("oracle requires a symmetric matrix")
-    dev = torch.device(f"cuda:{device}")
-    ta = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return a
+
+
+def _eigh_device(a: np.ndarray, device: int):
+    """Full symmetric eigendecomposition on the GPU (cuSOLVER) with the
+    reference's residual acceptance (oracle.py:58-63); host (lam, vec)."""
+    import torch
+
+    ta = torch.from_numpy(np.ascontiguousarray(a)).to(torch.device(f"cuda:{device}"))
     lam, vec = torch.linalg.eigh(ta)
     residual = float((ta @ vec - vec * lam).abs().max()) if a.size else 0.0
     if residual > EIG_RESIDUAL_TOL:
         raise OracleError(f"eigensolver residual {residual:.3e} above {EIG_RESIDUAL_TOL}")
-    lam_h = lam.cpu().numpy()
-    weights = np.atleast_1d(np.asarray(f(lam_h), dtype=np.float64))
+    return lam.cpu().numpy(), vec.cpu().numpy()
+
+
+def _pairwise_distances(rows: np.ndarray, device: int) -> np.ndarray:
+    """Upper-triangle pairwise Euclidean distances, the reference's formula
+    sqrt(max(|x|^2 + |y|^2 - 2 x.y, 0)) (oracle.py:219-224), in fp64 on the GPU."""
+    import torch
+
+    x = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.float64)).to(torch.device(f"cuda:{device}"))
+    sq = (x * x).sum(dim=1)
+    d2 = sq[:, None] + sq[None, :] - 2.0 * (x @ x.T)
+    iu = torch.triu_indices(x.shape[0], x.shape[0], offset=1, device=x.device)
+    return torch.sqrt(torch.clamp(d2[iu[0], iu[1]], min=0.0))
+
+
+def distance_bound_audit(S, f, cfg, trials: int, cap: int = ORACLE_CAP, *, device: int = 0) -> float:
+    """Fraction of (trial, pair) events violating the two-sided distance bound
+    sqrt(1 -+ eps) * (exact distance -+ delta sqrt(2)) (oracle.py:196-216), where
+    delta is the expansion's worst error at the true eigenvalues.  Each trial
+    draws a fresh projection (the reference's hash, bit-identical) and embeds
+    through the device seam; exact spectrum and distances on the GPU."""
+    import math
+
+    import torch
+
+    a = _dense_symmetric(S, cap)
+    lam, vec = _eigh_device(a, device)
+    weights = np.atleast_1d(np.asarray(f(lam), dtype=np.float64))
+    expansion = legendre_coefficients(f, cfg.L)
+    delta = float(np.max(np.abs(weights - expansion_eval(expansion, lam)), initial=0.0))
+    d_exact = _pairwise_distances(vec * weights, device)
+    slack = delta * math.sqrt(2.0)
+    lower = math.sqrt(1.0 - cfg.epsilon) * (d_exact - slack)
+    upper = math.sqrt(1.0 + cfg.epsilon) * (d_exact + slack)
+    sp = SparseMatrix.from_dense(a)
+    n = a.shape[0]
+    violations = 0
+    for t in range(trials):
+        omega = sample_projection(n, cfg.d, fold_seed(cfg.seed, t), device=device)
+        emb = apply_expansion(sp, expansion, omega, device=device)
+        d_approx = _pairwise_distances(emb, device)
+        violations += int(torch.count_nonzero((d_approx < lower) | (d_approx > upper)))
+    return violations / (trials * d_exact.numel())
+
+
+def exact_embedding(S, f, cap: int = ORACLE_CAP, *, device: int = 0) -> ExactEmbedding:
+    """Exact embedding by a full dense symmetric eigendecomposition on the GPU
+    (oracle.py:46-71 semantics: square and symmetric to 1e-10, at most `cap`
+    rows, eigen-residual <= 1e-8, weights f(lambda), zero weights dropped)."""
+    a = _dense_symmetric(S, cap)
+    lam, vec = _eigh_device(a, device)
+    weights = np.atleast_1d(np.asarray(f(lam), dtype=np.float64))
     keep = weights != 0.0
-    emb = vec.cpu().numpy()[:, keep] * weights[keep]
-    return ExactEmbedding(embedding=emb, eigenvalues=lam_h)
+    return ExactEmbedding(embedding=vec[:, keep] * weights[keep], eigenvalues=lam)
 
 
 def _rows(x):

@@ -460,6 +460,26 @@ def cio_read(path):
     return cio.read_embedding(path)
 
 
+def gen_audit():
+    """oracle.distance_bound_audit (oracle.py:196-216): the violation fraction
+    for two settings on a small SBM (n=300, normalized adjacency scaled by 0.98)."""
+    from csemb import oracle as cor
+
+    edges, _ = sbm(300, 3, 0.2, 0.01, np.random.default_rng(41))
+    S = cs.scale_values(cs.normalized_adjacency(edges, 300), 0.98)  # spectrum strictly inside [-1, 1]
+    # (L, d, epsilon, trials, function): the identity is represented exactly
+    # (delta ~ 1e-16), so at small d the JL band is violated for a real share of pairs
+    cases = {"indicator": (40, 24, 0.5, 3, "indicator:0.5"), "identity_d8": (4, 8, 0.2, 3, "identity"),
+             "identity_d24": (6, 24, 0.3, 2, "identity")}
+    meta = {}
+    for name, (L, d, eps, trials, spec) in cases.items():
+        cfg = cs.EmbedConfig(L=L, d=d, seed=9, epsilon=eps)
+        f = cs.parse_function(spec)
+        meta[name] = {"L": L, "d": d, "epsilon": eps, "trials": trials, "function": spec, "seed": 9,
+                      "fraction": cor.distance_bound_audit(S, f, cfg, trials)}
+    _save("audit", meta, edges=edges.astype(np.int64))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -474,3 +494,4 @@ if __name__ == "__main__":
     gen_cli()
     gen_downstream()
     gen_cli_downstream()
+    gen_audit()

@@ -394,3 +394,16 @@ def test_nan_and_overflow_rows_follow_the_reference():
     labels, hist = O.kmeans(X, 1, seed=1)
     assert np.array_equal(a.labels, labels)
     assert len(a.inertia_history) == len(hist) and all(np.isnan(a.inertia_history)) == all(np.isnan(hist))
+
+
+def test_distance_bound_audit_vs_reference():
+    """oracle.distance_bound_audit on the device (cuSOLVER spectrum, device seam
+    embeddings, fp64 device distances) vs the reference's fractions
+    (tests/golden/audit.npz); pairs within ulps of a bound may flip (<= 3)."""
+    z, meta = load_golden("audit")
+    S = pb.scale_values(pb.normalized_adjacency(z["edges"], 300), 0.98)
+    n_pairs = 300 * 299 // 2
+    for name, m in meta.items():
+        cfg = pb.EmbedConfig(L=m["L"], d=m["d"], seed=m["seed"], epsilon=m["epsilon"])
+        got = D.distance_bound_audit(S, pb.parse_function(m["function"]), cfg, m["trials"])
+        assert abs(got - m["fraction"]) * m["trials"] * n_pairs <= 3, (name, got, m["fraction"])
