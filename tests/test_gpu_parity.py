@@ -751,3 +751,34 @@ def test_repeated_create_destroy_does_not_grow_memory(config1):
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20, (free0, free1)
     assert sha(first) == meta["E_sha256"]
+
+
+@pytest.mark.parametrize("kind,n,d,L,row_order", [
+    ("sbm", 200_000, 80, 6, -1),        # windowed batch-count buckets (auto)
+    ("sbm", 150_000, 24, 7, 2),         # windowed, narrow rows (G = 4)
+    ("chung_lu", 200_000, 40, 6, -1),   # skewed: global buckets (auto)
+    ("chung_lu", 120_000, 130, 5, 4096),  # explicit window, column tiling
+    ("random", 150_000, 8, 6, 1),       # global buckets on a uniform graph
+])
+def test_schedule_orders_bit_exact_at_scale(kind, n, d, L, row_order):
+    """Medium-scale bit-exactness of the fused recurrence under every row
+    schedule (windowed / global batch-count buckets, natural), f64, against
+    the C oracle.  Row splitting off so every row keeps stored order."""
+    if kind == "sbm":
+        S = graphs.sbm(n, 20, 12.0, 4.0, seed=n)
+    elif kind == "chung_lu":
+        S = graphs.chung_lu(n, seed=3)
+    else:
+        rng = np.random.default_rng(n)
+        S = pb.normalized_adjacency(rng.integers(0, n, size=(8 * n, 2)), n)
+    th = pb.legendre_coefficients(pb.indicator_above(0.6), L).coeffs
+    om = O.sample_projection(n, d, 5)
+    ref = _oracle_embed(S, th, om)
+    dm = pb.DeviceMatrix(S, "float64")
+    plan = dm.plan(d)
+    plan.set_load_balance(split_threshold=0, row_order=row_order)
+    got = plan.apply(th, 1, om)
+    assert np.array_equal(got, ref)
+    plan.set_load_balance(row_order=0)
+    assert np.array_equal(plan.apply(th, 1, om), ref)
+    dm.close()
