@@ -122,6 +122,47 @@ def ncu_traffic(dtype: str):
         return None
 
 
+def gather_ceilings(dtype: str):
+    """Random row-gather bandwidth of K1's row width (tools/membench.cu,
+    profiles/r1_membench.txt): 640-byte rows (f64 d=80) / 320-byte rows (f32),
+    L2-resident (48 MB window) and spread over a window the size of Q(r-1)."""
+    tag, win = ("gather640", 640) if dtype == "f64" else ("gather320", 320)
+    out = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_membench.txt")) as fh:
+            for line in fh:
+                f = line.split()
+                if f and f[0] == tag and "nc" in f:
+                    out[int(f[1])] = float(f[f.index("nc") + 1])
+    except (OSError, ValueError, IndexError):
+        return None
+    return (out[48], out[win], win) if 48 in out and win in out else None
+
+
+def gather_roof(nnz: int, ld: int, dtype: str, k1_ms: float):
+    """K1's L2->SM side: every stored entry gathers one ld-wide row of Q(r-1)
+    (T*ld*dtype bytes per launch, 3.7x the algorithmic HBM bytes on config 2).
+    Model time = hit share at the L2-resident gather rate + miss share at the
+    Q(r-1)-sized-window rate, with K1's L2 hit rate from the committed ncu capture."""
+    es = 8 if dtype == "f64" else 4
+    gb = nnz * ld * es
+    roof = {"bytes_per_launch": gb, "l2_to_sm_gbs": round(gb / (k1_ms * 1e-3) / 1e9, 1)}
+    ceil = gather_ceilings(dtype)
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            hit = json.load(fh)["l2_hit_rate"][dtype]
+    except (OSError, KeyError, ValueError):
+        hit = None
+    if ceil and hit is not None:
+        res, wide, win = ceil
+        t_model = gb * (hit / (res * 1e9) + (1 - hit) / (wide * 1e9))
+        roof.update({"ceiling_l2_resident_gbs": res, f"ceiling_{win}MB_window_gbs": wide,
+                     "l2_hit_rate": hit, "model_ms": round(t_model * 1e3, 4),
+                     "frac_of_model": round(t_model / (k1_ms * 1e-3), 3),
+                     "source": "profiles/r1_membench.txt (max clocks), profiles/k1_traffic.json"})
+    return roof
+
+
 def k1_bytes(nnz: int, n: int, d: int, ld: int, dtype: str) -> int:
     """north_star model: T*(idx+val) + 5*n*d*dtype (Y_l, Y_{l-1}, E read; Y_{l+1}, E written)."""
     es = 8 if dtype == "f64" else 4
@@ -208,6 +249,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             roof["dram"] = {"gbs": round(dram_gbs, 1), "frac_of_8000": round(dram_gbs / 8000.0, 4),
                             "frac_of_measured": round(dram_gbs / peak, 4),
                             "traffic_over_model": round(traffic / B, 3)}
+        W = 2 if dtype == "f64" else 4
+        roof["gather"] = gather_roof(nnz, (hi - lo + W - 1) // W * W, dtype, k1_ms)
         out = {
             "value": units / (ms * 1e-3), "ms_per_step": ms, "k1_ms": k1_ms,
             "gpu_launches_per_step": launches_per_step,

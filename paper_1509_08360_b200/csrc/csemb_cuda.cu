@@ -266,7 +266,13 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
             H.partials = partials;
             H.n_heavy = sc->n_heavy;
             const int grid = grid_for((int64_t)sc->n_heavy * 32, 256, sm, 8);
-            k_heavy_combine<T, MODE, PEAK><<<grid, 256, 0, s>>>(P, H);
+            const int ms = (P.nvt + 31) / 32;
+            if (ms <= 1)
+                k_heavy_combine<T, MODE, PEAK, 1><<<grid, 256, 0, s>>>(P, H);
+            else if (ms == 2)
+                k_heavy_combine<T, MODE, PEAK, 2><<<grid, 256, 0, s>>>(P, H);
+            else
+                k_heavy_combine<T, MODE, PEAK, 3><<<grid, 256, 0, s>>>(P, H);
             e = cudaGetLastError();
             if (e != cudaSuccess) return e;
             ++nl;

@@ -611,11 +611,14 @@ struct HeavyParams {
     int n_heavy;
 };
 
-template <typename T, int MODE, int PEAK>
+template <typename T, int MODE, int PEAK, int MS>
 __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const HeavyParams H) {
     typedef typename Vec<T>::type VT;
     constexpr int W = Vec<T>::W;
-    constexpr int MS = 3;  // vectors per lane: a tile has at most 96 vectors
+    // MS vectors per lane (a tile has at most 96 vectors); U chunk partials in
+    // flight per lane: the longest heavy rows (10^6 entries, ~2000 chunks) set
+    // this kernel's time, one dependent round of loads per U chunks
+    constexpr int U = MS == 1 ? 24 : (MS == 2 ? 12 : 8);
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -638,17 +641,17 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
         VT acc[MS];
 #pragma unroll
         for (int k = 0; k < MS; ++k) acc[k] = vzero(VT());
-        // chunk partials in chunk order; 8 chunks' loads in flight at a time
+        // chunk partials in chunk order; U chunks' loads in flight at a time
         int c = c0;
-        for (; c + 8 <= c1; c += 8) {
-            VT x[8][MS];
+        for (; c + U <= c1; c += U) {
+            VT x[U][MS];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int k = 0; k < MS; ++k)
                     x[u][k] = valid[k] ? part[(int64_t)(c + u) * P.ldv + 32 * k] : vzero(VT());
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int k = 0; k < MS; ++k)
                     if (valid[k]) acc[k] = vmadd(acc[k], (T)1, x[u][k]);

@@ -65,6 +65,31 @@ __global__ void k_gather_rows(const float4 *__restrict__ a, uint32_t nrows, uint
     if (acc == 1234.5f) *sink = acc;
 }
 
+// 8 lanes per 320-byte row (f32 d=80): lane l reads vectors l, l+8 and (l < 4) l+16
+__global__ void k_gather_rows320(const float4 *__restrict__ a, uint32_t nrows, uint32_t iters, float *sink) {
+    const uint32_t lane = threadIdx.x & 7;
+    uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    uint32_t h = g * 2654435761u + 12345u;
+    float acc = 0.f;
+    for (uint32_t it = 0; it < iters; it += 2) {
+        float4 v[2][3];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            h = h * 1664525u + 1013904223u;
+            const uint32_t row = (uint32_t)(((uint64_t)(h >> 3) * nrows) >> 29);
+            const float4 *p = a + (size_t)row * 20 + lane;
+            v[u][0] = __ldg(p);
+            v[u][1] = __ldg(p + 8);
+            v[u][2] = lane < 4 ? __ldg(p + 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) acc += v[u][k].x + v[u][k].w;
+    }
+    if (acc == 1234.5f) *sink = acc;
+}
+
 template <int CG, int UNROLL>
 __global__ void k_gather(const float4 *__restrict__ a, uint32_t nrows, uint32_t iters, float *sink) {
     const uint32_t lane = threadIdx.x & 7;
@@ -162,6 +187,14 @@ int main() {
         float ms2 = best_ms([&] { k_gather_rows<2, 5><<<grid, block>>>(a, nrows, it2, sink); });
         printf("gather640 %4zu MB: %s %.0f  %s %.0f  %s %.0f GB/s\n", mb, names[0], gb2 / ms0 / 1e6, names[1],
                gb2 / ms1 / 1e6, names[2], gb2 / ms2 / 1e6);
+    }
+    // 320-byte rows (f32 d=80, K1's fp32 gather), ld.global.nc
+    for (size_t mb : {48, 320, 2048}) {
+        uint32_t nrows = (uint32_t)((mb << 20) / 320);
+        const uint32_t it2 = 64;
+        const double gb2 = (double)lanes_total / 8 * it2 * 320;
+        float ms0 = best_ms([&] { k_gather_rows320<<<grid, block>>>(a, nrows, it2, sink); });
+        printf("gather320 %4zu MB: nc %.0f GB/s\n", mb, gb2 / ms0 / 1e6);
     }
     return 0;
 }
