@@ -168,6 +168,20 @@ int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int order, int n_
  * so the assembled E is bit-identical to the single-GPU run.  */
 int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev, void *q0_dev,
                          void *q1_dev);
+/* Fused exchange over peer memory (instead of an all-gather between steps).
+ * full0_dev / full1_dev: this rank's two replicated n_global x ld buffers;
+ * Q(r) lives in parity r & 1.  peer_full0[i] / peer_full1[i]: the same two
+ * buffers of peer i, mapped into this process (CUDA IPC / torch symmetric
+ * memory over NVLink); n_peer <= 15.  Step r gathers from full[(r-1) & 1]
+ * and its epilogue stores each Q(r) row in place into this rank's rows of
+ * full[r & 1] AND into the same rows of every peer's full[r & 1], so the
+ * exchange overlaps the step.  The caller places one barrier across ranks
+ * after each step (all of Q(r) delivered, all reads of Q(r-1) done) and before
+ * the next.  Generated projections only (SPLITMIX / PHILOX); results are
+ * bit-identical to the all-gather variant and to one GPU.  */
+int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
+                               void *full1_dev, int n_peer, void *const *peer_full0,
+                               void *const *peer_full1);
 /* Stage init for the local rows (hash of the GLOBAL row index); for generated
  * kinds also writes the full Q(0) into full_dev (no exchange before step 1). */
 int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, const double *block_dev,

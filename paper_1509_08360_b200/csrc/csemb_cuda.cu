@@ -64,6 +64,12 @@ struct csemb_plan {
     int64_t row0 = 0, n_global = 0;
     void *full = nullptr;
     void *ext_q[2] = {nullptr, nullptr};
+    // fused exchange (csemb_plan_partition_peers): two replicated full buffers
+    // (Q(r) lives in full2[r & 1]) and the peers' buffers of each parity
+    bool fused = false;
+    void *full2[2] = {nullptr, nullptr};
+    int n_peer = 0;
+    void *peer_full[2][K1_MAX_PEERS] = {};
     std::vector<double> coeffs;  // stage coefficients of the step-wise run
     int64_t col0 = 0, d_global = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -121,9 +127,9 @@ static int use_tma() {
     return on;
 }
 
-template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED>
+template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED, int PEERS = 0>
 static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count) {
-    const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK, STAGED>;
+    const void *fn = (const void *)k_step<T, G, VPL, MODE, PEAK, STAGED, PEERS>;
     const int threads = 256;
     const int W = Vec<T>::W;
     const int nch = ((P0.col0 + (P0.v0 + P0.nvt) * W - 1) >> 5) - ((P0.col0 + P0.v0 * W) >> 5) + 1;
@@ -157,7 +163,7 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
         per_sm = it->second;
     }
     const int grid = grid_for(P.n_rows * G, threads, sm_count, per_sm);
-    k_step<T, G, VPL, MODE, PEAK, STAGED><<<grid, threads, smem, s>>>(P);
+    k_step<T, G, VPL, MODE, PEAK, STAGED, PEERS><<<grid, threads, smem, s>>>(P);
     return cudaGetLastError();
 }
 
@@ -166,6 +172,10 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
     if constexpr (G >= 8) {
         if (use_tma() == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
         if (use_tma() == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
+    }
+    // fused row-partition exchange: peer stores in the epilogue (PEAK_FLAG steps)
+    if constexpr (MODE == MODE_RECUR && PEAK == PEAK_FLAG) {
+        if (P.n_peer) return run_step_t<T, G, VPL, MODE, PEAK, 0, 1>(P, s, sm_count);
     }
     return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
 }
@@ -245,6 +255,7 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
             C.E = nullptr;
             C.reverse = 0;
             C.peaks = nullptr;
+            C.n_peer = 0;  // chunk partial sums stay local
             e = dispatch_group<T, MODE_SPMM, PEAK_FLAG>(G, vpl, C, s, sm);
             if (e != cudaSuccess) return e;
             ++nl;
@@ -974,6 +985,8 @@ static int plan_run_locked(csemb_plan *p, const double *coeffs, int order, int n
         return fail(CSEMB_ERR_INVALID, "unknown omega kind %d", omega_kind);
     if (omega_kind == CSEMB_OMEGA_GIVEN && !block_dev && p->m->n_rows > 0)
         return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
+    if (omega_kind == CSEMB_OMEGA_GIVEN && p->fused)
+        return fail(CSEMB_ERR_UNSUPPORTED, "the fused exchange generates Q(0) on every rank (SPLITMIX or PHILOX)");
     if (d_global < p->d || col0 < 0 || col0 + p->d > d_global)
         return fail(CSEMB_ERR_INVALID, "column slice [%lld, %lld) outside d_global %lld", (long long)col0,
                     (long long)(col0 + p->d), (long long)d_global);
@@ -1213,6 +1226,34 @@ extern "C" int csemb_apply_expansion(csemb_plan *p, const double *coeffs, int or
 // ---------------------------------------------------------------------------
 // row-partitioned, step-wise runs (multi-GPU graphs larger than one GPU)
 // ---------------------------------------------------------------------------
+extern "C" int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
+                                          void *full1_dev, int n_peer, void *const *peer_full0,
+                                          void *const *peer_full1) {
+    if (!p || !full0_dev || !full1_dev) return fail(CSEMB_ERR_INVALID, "null argument");
+    if (n_peer < 0 || n_peer > K1_MAX_PEERS) return fail(CSEMB_ERR_INVALID, "n_peer must be in [0, %d]", K1_MAX_PEERS);
+    if (n_peer > 0 && (!peer_full0 || !peer_full1)) return fail(CSEMB_ERR_INVALID, "null peer buffer list");
+    for (int i = 0; i < n_peer; ++i)
+        if (!peer_full0[i] || !peer_full1[i]) return fail(CSEMB_ERR_INVALID, "null peer buffer %d", i);
+    csemb_mat *m = p->m;
+    if (m->n_cols != n_global) return fail(CSEMB_ERR_INVALID, "local matrix must have n_global columns");
+    if (row0 < 0 || row0 + m->n_rows > n_global) return fail(CSEMB_ERR_INVALID, "row block outside [0, n_global)");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    p->partitioned = true;
+    p->fused = true;
+    p->row0 = row0;
+    p->n_global = n_global;
+    p->full2[0] = full0_dev;
+    p->full2[1] = full1_dev;
+    p->full = full0_dev;  // Q(0) is generated into parity 0
+    p->ext_q[0] = p->ext_q[1] = nullptr;
+    p->n_peer = n_peer;
+    for (int i = 0; i < n_peer; ++i) {
+        p->peer_full[0][i] = peer_full0[i];
+        p->peer_full[1][i] = peer_full1[i];
+    }
+    return CSEMB_OK;
+}
+
 extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev,
                                     void *q0_dev, void *q1_dev) {
     if (!p || !full_dev) return fail(CSEMB_ERR_INVALID, "null argument");
@@ -1222,6 +1263,8 @@ extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_globa
     if ((q0_dev == nullptr) != (q1_dev == nullptr)) return fail(CSEMB_ERR_INVALID, "give both local buffers or neither");
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     p->partitioned = true;
+    p->fused = false;
+    p->n_peer = 0;
     p->row0 = row0;
     p->n_global = n_global;
     p->full = full_dev;
@@ -1252,7 +1295,7 @@ static int plan_begin_t(csemb_plan *p, const double *block_dev, int omega_kind, 
     p->n_stages = 1;
     p->n_chunks = n_chunks;
     p->step_launches = 0;
-    T *q0 = (T *)(p->ext_q[0] ? p->ext_q[0] : p->y[0]);
+    T *q0 = p->fused ? (T *)p->full2[0] + p->row0 * (int64_t)ld : (T *)(p->ext_q[0] ? p->ext_q[0] : p->y[0]);
     const double scale = 1.0 / std::sqrt((double)p->d_global);
     CK(cudaEventRecord(p->ev[0], s));
     if (n > 0)
@@ -1276,6 +1319,8 @@ extern "C" int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, 
         return fail(CSEMB_ERR_INVALID, "unknown omega kind %d", omega_kind);
     if (omega_kind == CSEMB_OMEGA_GIVEN && !block_dev && p->m->n_rows > 0)
         return fail(CSEMB_ERR_INVALID, "omega_kind GIVEN needs a block");
+    if (omega_kind == CSEMB_OMEGA_GIVEN && p->fused)
+        return fail(CSEMB_ERR_UNSUPPORTED, "the fused exchange generates Q(0) on every rank (SPLITMIX or PHILOX)");
     if (d_global < p->d || col0 < 0 || col0 + p->d > d_global || col0 % vec_w(p->m->dtype) != 0)
         return fail(CSEMB_ERR_INVALID, "bad column slice");
     for (int r = 0; r <= order; ++r)
@@ -1312,8 +1357,20 @@ static int plan_step_t(csemb_plan *p, int r) {
     P.rowptr = m->rowptr;
     P.cols = m->cols;
     P.vals = m->vals;
-    P.ycur = p->full;  // full Q(r-1), refreshed by the caller's all-gather
-    P.yout = p->ext_q[r & 1] ? p->ext_q[r & 1] : p->y[r & 1];
+    if (p->fused) {
+        // Q(r-1) in full2[(r-1) & 1], written by every rank's step r-1; Q(r)
+        // overwrites this rank's rows of Q(r-2) in full2[r & 1] in place and is
+        // stored into the same rows of every peer's full2[r & 1]
+        P.ycur = p->full2[(r - 1) & 1];
+        P.yout = (T *)p->full2[r & 1] + p->row0 * p->ld;
+        P.n_peer = p->n_peer;
+        for (int i = 0; i < p->n_peer; ++i) P.peer[i] = p->peer_full[r & 1][i];
+        if (p->exact_peaks && p->n_peer)
+            return fail(CSEMB_ERR_UNSUPPORTED, "exact per-step peaks are not combined with the fused exchange");
+    } else {
+        P.ycur = p->full;  // full Q(r-1), refreshed by the caller's all-gather
+        P.yout = p->ext_q[r & 1] ? p->ext_q[r & 1] : p->y[r & 1];
+    }
     P.E = p->E;
     P.n_rows = n;
     P.ldv = ldv;

@@ -122,6 +122,10 @@ __device__ __forceinline__ unsigned long long vpeak(float4 q) {
 template <typename V> __device__ __forceinline__ V ld_stream(const V *p) { return __ldcs(p); }
 template <typename V> __device__ __forceinline__ void st_stream(V *p, V v) { __stcs(p, v); }
 
+#ifndef K1_MAX_PEERS
+#define K1_MAX_PEERS 15  // remote replicas a step can write (16 ranks)
+#endif
+
 struct StepParams {
     const int64_t *rowptr;
     const int *cols;
@@ -152,6 +156,12 @@ struct StepParams {
     const int *perm;
     const int64_t *rbeg;
     const int64_t *rend;
+    // fused exchange of the row partition (csemb_plan_partition_peers): every
+    // Q(r) row is also stored, at its GLOBAL row, into each peer's replicated
+    // full buffer over NVLink (P2P), so the transfer overlaps the step instead
+    // of following it as an all-gather
+    void *peer[K1_MAX_PEERS];
+    int n_peer;
 };
 
 // Per-chunk diagnostics.  PEAK_EXACT keeps, per lane slot, the running max of
@@ -278,7 +288,7 @@ __device__ __forceinline__ void tma_row(void *dst, const void *src, unsigned byt
 // -- or the next row's first batch -- are loaded while the current batch's
 // gathers are outstanding.  Streamed data (entries, Q(r-2), E) is read
 // evict-first so L2 keeps the gathered rows of Q(r-1).
-template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED = 0>
+template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED = 0, int PEERS = 0>
 __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_step(const StepParams P) {
     extern __shared__ __align__(128) unsigned char k1_dyn_smem[];
     typedef typename Vec<T>::type VT;
@@ -547,6 +557,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
 #else
                         yo[k * G] = q;
 #endif
+                        if constexpr (PEERS) {  // the same row of every peer's full Q(r) buffer
+                            const int64_t off = (P.row_base + row) * (int64_t)P.ldv + P.v0 + gl + k * G;
+                            for (int pi = 0; pi < P.n_peer; ++pi) reinterpret_cast<VT *>(P.peer[pi])[off] = q;
+                        }
                         if (P.efold) {  // ((E + th2*Q(r-2)) + th1*Q(r-1)) + th*Q(r), the reference's order
                             VT e = ev[k];
                             if (P.efold & 4) e = vaccum(e, theta2, pv[k]);
@@ -571,6 +585,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     }
 
     if constexpr (STAGED == 2) cp_async_wait<0>();
+    if constexpr (PEERS) __threadfence_system();  // peer stores performed before the step's barrier
     if (MODE == MODE_RECUR && P.peaks) {
         // per-chunk max over the block, then one atomic per chunk per block
         unsigned long long *s_peak = reinterpret_cast<unsigned long long *>(k1_dyn_smem);
@@ -676,6 +691,8 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
             const VT p = has_prev ? ld_stream(yo + 32 * k) : vzero(VT());
             const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
             yo[32 * k] = q;
+            for (int pi = 0; pi < P.n_peer; ++pi)  // fused exchange (see StepParams::peer)
+                reinterpret_cast<VT *>(P.peer[pi])[(P.row_base + row) * (int64_t)P.ldv + P.v0 + lane + 32 * k] = q;
             if (P.efold) {
                 VT e = ld_stream(er + 32 * k);
                 if (P.efold & 4) e = vaccum(e, (T)P.theta2, p);
@@ -690,6 +707,7 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
             }
         }
     }
+    if (P.n_peer) __threadfence_system();
     if (MODE == MODE_RECUR && P.peaks) {
 #pragma unroll
         for (int k = 0; k < MS; ++k) {

@@ -131,12 +131,15 @@ class DeviceRowEngine:
     """One rank's share of a row-partitioned run on its GPU (C ABI step-wise
     plan over caller-owned torch buffers)."""
 
-    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q):
+    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q, peers=None):
         from .engine import DeviceMatrix
 
         self.dm = DeviceMatrix(S_local, "float64" if dtype == "f64" else "float32", device)
         self.plan = self.dm.plan(d)
-        self.plan.partition(row0, n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        if peers is None:
+            self.plan.partition(row0, n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        else:  # fused exchange: F = this rank's two full buffers, peers = (parity-0, parity-1) pointer lists
+            self.plan.partition_peers(row0, n_global, (F[0].data_ptr(), F[1].data_ptr()), peers[0], peers[1])
         self.n_local, self.d = S_local.n_rows, d
 
     def begin(self, coeffs, omega_kind, seed, col0, d_global):
@@ -159,9 +162,29 @@ class DeviceRowEngine:
         return out, peaks
 
 
+def peer_buffers(shape, dtype, device, group):
+    """Two replicated full buffers in torch symmetric memory (NVLink-mapped on
+    every rank) and, per parity, the device pointers of the peers' copies."""
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    group = dist.group.WORLD if group is None else group
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    F, peers = [], ([], [])
+    for parity in range(2):
+        t = symm_mem.empty(*shape, dtype=dtype, device=device)
+        t.zero_()
+        hdl = symm_mem.rendezvous(t, group)
+        F.append(t)
+        for p in range(world):
+            if p != rank:
+                peers[parity].append(hdl.get_buffer(p, list(shape), dtype).data_ptr())
+    return F, peers
+
+
 def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, seed: int = 0,
                           omega_kind: str = "reference", dtype: str = "f64", normalize_rows: bool = False,
-                          group=None, device: int | None = None, engine_factory=None):
+                          group=None, device: int | None = None, engine_factory=None, exchange: str = "allgather"):
     """E rows [row0, row0 + n_local) of f_L(S) Omega for a row-partitioned S.
 
     Each rank holds its row block of S (global column ids); every step gathers
@@ -171,6 +194,11 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     exchange precedes step 1.  Per-row arithmetic is unchanged, so the
     assembled E is bit-identical to the single-GPU result.  Returns the local
     E rows (torch tensor) and the per-chunk diagnostics max-combined over ranks.
+
+    exchange="allgather": one NCCL all-gather of the local Q(r) per step.
+    exchange="peer": the fused exchange -- K1's epilogue stores every Q(r) row
+    into all ranks' replicated buffers over NVLink (torch symmetric memory),
+    so the transfer overlaps the step; one barrier per step.  GPU only.
     """
     import torch
     import torch.distributed as dist
@@ -189,6 +217,23 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     on_gpu = engine_factory is None
     dev = torch.device(f"cuda:{torch.cuda.current_device() if device is None else device}") if on_gpu \
         else torch.device("cpu")
+    if exchange not in ("allgather", "peer"):
+        raise ValueError("exchange must be 'allgather' or 'peer'")
+    if exchange == "peer":
+        if not on_gpu:
+            raise ValueError("the fused peer exchange runs on GPUs (torch symmetric memory)")
+        F2, peers = peer_buffers((world * n_pad, ld), tdt, dev, group)
+        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F2, None, peers=peers)
+        kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
+        eng.begin(coeffs, kind, seed, 0, d)
+        flag = torch.zeros(1, device=dev)
+        for r in range(1, len(coeffs)):
+            eng.step(r)  # host-synchronous: this rank's stores of Q(r) are complete
+            if r < len(coeffs) - 1:  # every rank done with step r before any starts step r+1
+                dist.all_reduce(flag, group=group)
+                torch.cuda.synchronize(dev)
+        E, peaks = eng.end(normalize_rows)
+        return E, combine_peaks(peaks, group)
     F = torch.zeros((world * n_pad, ld), dtype=tdt, device=dev)
     q = [torch.zeros((n_pad, ld), dtype=tdt, device=dev) for _ in range(2)]
     if on_gpu:

@@ -321,6 +321,17 @@ class Plan:
             None if q0_ptr is None else C.c_void_p(q0_ptr), None if q1_ptr is None else C.c_void_p(q1_ptr)),
             "csemb_plan_partition")
 
+    def partition_peers(self, row0: int, n_global: int, full_ptrs, peer_ptrs0=(), peer_ptrs1=()) -> None:
+        """Fused exchange: this rank's two full buffers and the peers' (same order)."""
+        n = len(peer_ptrs0)
+        if len(peer_ptrs1) != n:
+            raise ValueError("give both parities of every peer buffer")
+        arr0 = (C.c_void_p * max(n, 1))(*[C.c_void_p(int(x)) for x in peer_ptrs0])
+        arr1 = (C.c_void_p * max(n, 1))(*[C.c_void_p(int(x)) for x in peer_ptrs1])
+        _lib.check(self.lib.csemb_plan_partition_peers(
+            self.handle, int(row0), int(n_global), C.c_void_p(int(full_ptrs[0])), C.c_void_p(int(full_ptrs[1])),
+            n, arr0, arr1), "csemb_plan_partition_peers")
+
     def begin(self, coeffs, *, block_dev: int | None = None, omega_kind: int = _lib.OMEGA_SPLITMIX, seed: int = 0,
               col0: int = 0, d_global: int | None = None) -> None:
         c = np.ascontiguousarray(coeffs, dtype=np.float64)

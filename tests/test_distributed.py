@@ -180,3 +180,35 @@ def test_row_blocks():
 
     assert row_blocks(10, 3) == (4, [(0, 4), (4, 8), (8, 10)])
     assert row_blocks(2, 4) == (1, [(0, 1), (1, 2), (2, 2), (2, 2)])
+
+
+def _exchange_arg_worker(rank, world, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import embed_row_partitioned, local_rows, row_blocks
+
+        S, coeffs = _problem()
+        _, blocks = row_blocks(S.n_rows, world)
+        lo, hi = blocks[rank]
+        Sl = local_rows(_as_sparse(S), lo, hi)
+        msgs = []
+        for exchange in ("peer", "ring"):  # peer: GPUs only (symmetric memory); ring: unknown
+            try:
+                embed_row_partitioned(Sl, lo, S.n_rows, coeffs, 8, engine_factory=OracleRowEngine, exchange=exchange)
+                msgs.append("no error")
+            except ValueError as e:
+                msgs.append(str(e))
+        with open(result_path + f".{rank}.txt", "w") as fh:
+            fh.write("\n".join(msgs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_partitioned_exchange_argument(tmp_path):
+    out = str(tmp_path / "ex")
+    mp.start_processes(_exchange_arg_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn", join=True)
+    for p in range(2):
+        msgs = open(out + f".{p}.txt").read().split("\n")
+        assert "GPUs" in msgs[0] and "exchange must be" in msgs[1]

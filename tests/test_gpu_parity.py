@@ -263,6 +263,28 @@ class TestEdgeCases:
         assert rel(plan.apply(th, 1, om), ref) <= 1e-13
         plan.set_load_balance(split_threshold=4096)
 
+    def test_heavy_combine_many_chunks(self):
+        # a 59999-entry hub row = 59 chunks of 1024: the combine's unrolled rounds
+        # (24 / 12 / 8 chunks in flight for tiles of <= 32 / 64 / 96 vectors) and
+        # its remainder loop, for each width class, in both dtypes
+        n = 60000
+        rng = np.random.default_rng(11)
+        e = np.concatenate([np.stack([np.zeros(n - 1, np.int64), np.arange(1, n)], 1),
+                            rng.integers(0, n, size=(120000, 2))])
+        S = pb.normalized_adjacency(e, n)
+        th = pb.legendre_coefficients(pb.commute_time(0.01), 6).coeffs
+        dm, dm32 = pb.DeviceMatrix(S), pb.DeviceMatrix(S, "float32")
+        for d in (40, 100, 180):  # fp64 tiles of 20 / 50 / 90 vectors
+            om = O.sample_projection(n, d, d)
+            ref = _oracle_embed(S, th, om)
+            plan = dm.plan(d)
+            got = plan.apply(th, 1, om)
+            assert rel(got, ref) <= 1e-13, d
+            assert np.array_equal(plan.apply(th, 1, om), got), d  # deterministic
+            assert rel(dm32.plan(d).apply(th, 1, om), ref) <= FP32_REL, d
+        dm.close()
+        dm32.close()
+
     def test_row_order_is_bit_identical(self):
         import scipy.sparse as sp  # noqa: F401
 
@@ -463,6 +485,78 @@ class TestRowPartition:
             dm.close()
         assert np.array_equal(np.concatenate(got), ref)
 
+    @pytest.mark.parametrize("dtype", ["float64", "float32"])
+    def test_fused_peer_exchange_emulated(self, dtype):
+        # csemb_plan_partition_peers: each "rank" stores its Q(r) rows into the
+        # other ranks' replicated buffers from K1's epilogue (here: buffers on
+        # the same GPU standing in for NVLink-mapped peers).  Ranks never wait
+        # on one another; the per-step barrier is a host sync of every rank.
+        import torch
+
+        from paper_1509_08360_b200.distributed import local_rows, row_blocks
+
+        S = graphs.sbm(3001, 7, 10.0, 3.0, seed=4)
+        n, d, L = S.n_rows, 40, 12
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), L).coeffs
+        ref = pb.DeviceMatrix(S, dtype).plan(d).apply(th, 1, None, omega_kind=1, seed=3)
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        world = 3
+        n_pad, blocks = row_blocks(n, world)
+        F = [[torch.zeros((world * n_pad, d), dtype=tdt, device="cuda") for _ in range(2)] for _ in range(world)]
+        torch.cuda.synchronize()
+        ranks = []
+        for p, (lo, hi) in enumerate(blocks):
+            dm = pb.DeviceMatrix(local_rows(S, lo, hi), dtype)
+            plan = dm.plan(d)
+            others = [q for q in range(world) if q != p]
+            plan.partition_peers(lo, n, (F[p][0].data_ptr(), F[p][1].data_ptr()),
+                                 [F[q][0].data_ptr() for q in others], [F[q][1].data_ptr() for q in others])
+            plan.begin(th, omega_kind=1, seed=3)
+            ranks.append((dm, plan))
+        for dm, _ in ranks:
+            dm.ctx.sync()
+        for r in range(1, L + 1):
+            for _, plan in ranks:
+                plan.step(r)
+            for dm, _ in ranks:  # the per-step barrier
+                dm.ctx.sync()
+        got = []
+        for dm, plan in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        assert np.array_equal(np.concatenate(got), ref)
+        # every replica holds the whole final Q(L) (parity L & 1), identical across ranks
+        torch.cuda.synchronize()
+        for p in range(1, world):
+            assert torch.equal(F[p][L & 1][:n], F[0][L & 1][:n])
+
+    def test_fused_peer_exchange_errors(self):
+        S = graphs.sbm(500, 2, 6.0, 2.0, seed=1)
+        dm = pb.DeviceMatrix(S)
+        plan = dm.plan(8)
+        import torch
+
+        F = [torch.zeros((500, 8), dtype=torch.float64, device="cuda") for _ in range(2)]
+        with pytest.raises(ValueError):
+            plan.partition_peers(0, 500, (F[0].data_ptr(), F[1].data_ptr()), [F[0].data_ptr()], [])
+        with pytest.raises(ValueError):
+            plan.partition_peers(0, 500, (F[0].data_ptr(), F[1].data_ptr()), [0], [0])
+        with pytest.raises(ValueError):
+            plan.partition_peers(0, 500, (F[0].data_ptr(), F[1].data_ptr()), [F[0].data_ptr()] * 16,
+                                 [F[1].data_ptr()] * 16)
+        plan.partition_peers(0, 500, (F[0].data_ptr(), F[1].data_ptr()))
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), 3).coeffs
+        with pytest.raises(NotImplementedError):  # the fused exchange generates Q(0) itself
+            plan.begin(th, block_dev=F[0].data_ptr(), omega_kind=0)
+        plan.begin(th, omega_kind=1, seed=5)
+        for r in range(1, 4):
+            plan.step(r)
+        plan.end(False)
+        ref = pb.DeviceMatrix(S).plan(8).apply(th, 1, None, omega_kind=1, seed=5)
+        assert np.array_equal(plan.download(), ref)
+        dm.close()
+
     def test_nccl_driver_world_one(self):
         import socket
 
@@ -482,6 +576,9 @@ class TestRowPartition:
             ref, _, _ = O.run_stage(O.CSR.of(S), th, O.sample_projection(S.n_rows, 24, 2))
             assert np.array_equal(E.cpu().numpy(), ref)
             assert np.all(np.isfinite(peaks)) and not np.any(peaks >= np.inf)
+            # the fused exchange through torch symmetric memory (no peers at world 1)
+            E2, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="peer")
+            assert np.array_equal(E2.cpu().numpy(), ref)
         finally:
             dist.destroy_process_group()
 
