@@ -182,6 +182,13 @@ int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_global, void *fu
 int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
                                void *full1_dev, int n_peer, void *const *peer_full0,
                                void *const *peer_full1);
+/* Same exchange through NVLS multicast: mc0 / mc1 are the multicast addresses
+ * of full0 / full1 (a multicast object bound to every rank's replica, e.g.
+ * torch symmetric memory's multicast_ptr).  K1 stores each Q(r) row once
+ * (multimem.st) and the NVSwitch writes it into every replica, so each GPU
+ * sends its rows once instead of once per peer.  */
+int csemb_plan_partition_multicast(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
+                                   void *full1_dev, void *mc0, void *mc1);
 /* Stage init for the local rows (hash of the GLOBAL row index); for generated
  * kinds also writes the full Q(0) into full_dev (no exchange before step 1). */
 int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, const double *block_dev,

@@ -68,6 +68,7 @@ SIGNATURES = {
         _int, [_p, _p, _int, _int, _p, _int, _u64, _i64, _i64, _int, _p, _p, _pi, _pi]),
     "csemb_plan_partition": (_int, [_p, _i64, _i64, _p, _p, _p]),
     "csemb_plan_partition_peers": (_int, [_p, _i64, _i64, _p, _p, _int, _p, _p]),
+    "csemb_plan_partition_multicast": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
     "csemb_plan_begin": (_int, [_p, _p, _int, _p, _int, _u64, _i64, _i64]),
     "csemb_plan_step": (_int, [_p, _int]),
     "csemb_plan_end": (_int, [_p, _int]),

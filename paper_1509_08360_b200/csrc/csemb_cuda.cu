@@ -70,6 +70,7 @@ struct csemb_plan {
     void *full2[2] = {nullptr, nullptr};
     int n_peer = 0;
     void *peer_full[2][K1_MAX_PEERS] = {};
+    void *mc_full[2] = {nullptr, nullptr};  // NVLS multicast addresses of full2 (or null)
     std::vector<double> coeffs;  // stage coefficients of the step-wise run
     int64_t col0 = 0, d_global = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -175,6 +176,7 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
     }
     // fused row-partition exchange: peer stores in the epilogue (PEAK_FLAG steps)
     if constexpr (MODE == MODE_RECUR && PEAK == PEAK_FLAG) {
+        if (P.mc) return run_step_t<T, G, VPL, MODE, PEAK, 0, 2>(P, s, sm_count);
         if (P.n_peer) return run_step_t<T, G, VPL, MODE, PEAK, 0, 1>(P, s, sm_count);
     }
     return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
@@ -256,6 +258,7 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
             C.reverse = 0;
             C.peaks = nullptr;
             C.n_peer = 0;  // chunk partial sums stay local
+            C.mc = nullptr;
             e = dispatch_group<T, MODE_SPMM, PEAK_FLAG>(G, vpl, C, s, sm);
             if (e != cudaSuccess) return e;
             ++nl;
@@ -1251,6 +1254,18 @@ extern "C" int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n
         p->peer_full[0][i] = peer_full0[i];
         p->peer_full[1][i] = peer_full1[i];
     }
+    p->mc_full[0] = p->mc_full[1] = nullptr;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_partition_multicast(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
+                                              void *full1_dev, void *mc0, void *mc1) {
+    if (!mc0 || !mc1) return fail(CSEMB_ERR_INVALID, "null multicast address");
+    const int rc = csemb_plan_partition_peers(p, row0, n_global, full0_dev, full1_dev, 0, nullptr, nullptr);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    p->mc_full[0] = mc0;
+    p->mc_full[1] = mc1;
     return CSEMB_OK;
 }
 
@@ -1265,6 +1280,7 @@ extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_globa
     p->partitioned = true;
     p->fused = false;
     p->n_peer = 0;
+    p->mc_full[0] = p->mc_full[1] = nullptr;
     p->row0 = row0;
     p->n_global = n_global;
     p->full = full_dev;
@@ -1365,7 +1381,8 @@ static int plan_step_t(csemb_plan *p, int r) {
         P.yout = (T *)p->full2[r & 1] + p->row0 * p->ld;
         P.n_peer = p->n_peer;
         for (int i = 0; i < p->n_peer; ++i) P.peer[i] = p->peer_full[r & 1][i];
-        if (p->exact_peaks && p->n_peer)
+        P.mc = p->mc_full[r & 1];
+        if (p->exact_peaks && (p->n_peer || P.mc))
             return fail(CSEMB_ERR_UNSUPPORTED, "exact per-step peaks are not combined with the fused exchange");
     } else {
         P.ycur = p->full;  // full Q(r-1), refreshed by the caller's all-gather

@@ -162,7 +162,19 @@ struct StepParams {
     // of following it as an all-gather
     void *peer[K1_MAX_PEERS];
     int n_peer;
+    // ... or through one NVLS multicast address of the full Q(r) buffer (all
+    // ranks' replicas, this one included): one multimem store per 8 bytes that
+    // the NVSwitch replicates, instead of n_peer unicast stores
+    void *mc;
 };
+
+// bit-exact 16-byte store through a multicast address (two multimem.st.b64;
+// the vector forms take float types only)
+__device__ __forceinline__ void mc_store(void *p, const void *v16) {
+    const unsigned long long *w = reinterpret_cast<const unsigned long long *>(v16);
+    asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(w[0]) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"((char *)p + 8), "l"(w[1]) : "memory");
+}
 
 // Per-chunk diagnostics.  PEAK_EXACT keeps, per lane slot, the running max of
 // the |Q| bit patterns (the reference's logged max_abs, engine.py:217-220);
@@ -552,12 +564,17 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
 #if (K1_ABLATE & 4)
                         if (__double_as_longlong((double)vpeak(q)) == 12345) yo[k * G] = q;
 #else
+                        if constexpr (PEERS == 2) {  // every replica (this one too) through the multicast address
+                            const int64_t off = (P.row_base + row) * (int64_t)P.ldv + P.v0 + gl + k * G;
+                            mc_store(reinterpret_cast<VT *>(P.mc) + off, &q);
+                        } else {
 #if K1_QSTORE_CS
-                        st_stream(yo + k * G, q);
+                            st_stream(yo + k * G, q);
 #else
-                        yo[k * G] = q;
+                            yo[k * G] = q;
 #endif
-                        if constexpr (PEERS) {  // the same row of every peer's full Q(r) buffer
+                        }
+                        if constexpr (PEERS == 1) {  // the same row of every peer's full Q(r) buffer
                             const int64_t off = (P.row_base + row) * (int64_t)P.ldv + P.v0 + gl + k * G;
                             for (int pi = 0; pi < P.n_peer; ++pi) reinterpret_cast<VT *>(P.peer[pi])[off] = q;
                         }
@@ -585,6 +602,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     }
 
     if constexpr (STAGED == 2) cp_async_wait<0>();
+    if constexpr (PEERS == 2) asm volatile("fence.proxy.alias;" ::: "memory");  // multicast vs unicast aliases
     if constexpr (PEERS) __threadfence_system();  // peer stores performed before the step's barrier
     if (MODE == MODE_RECUR && P.peaks) {
         // per-chunk max over the block, then one atomic per chunk per block
@@ -690,9 +708,13 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
             if (!valid[k]) continue;
             const VT p = has_prev ? ld_stream(yo + 32 * k) : vzero(VT());
             const VT q = vrecur(acc[k], alpha, beta, p, has_prev);
-            yo[32 * k] = q;
-            for (int pi = 0; pi < P.n_peer; ++pi)  // fused exchange (see StepParams::peer)
-                reinterpret_cast<VT *>(P.peer[pi])[(P.row_base + row) * (int64_t)P.ldv + P.v0 + lane + 32 * k] = q;
+            const int64_t off = (P.row_base + row) * (int64_t)P.ldv + P.v0 + lane + 32 * k;
+            if (P.mc) {  // fused exchange (see StepParams::peer / mc)
+                mc_store(reinterpret_cast<VT *>(P.mc) + off, &q);
+            } else {
+                yo[32 * k] = q;
+                for (int pi = 0; pi < P.n_peer; ++pi) reinterpret_cast<VT *>(P.peer[pi])[off] = q;
+            }
             if (P.efold) {
                 VT e = ld_stream(er + 32 * k);
                 if (P.efold & 4) e = vaccum(e, (T)P.theta2, p);
@@ -707,7 +729,8 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
             }
         }
     }
-    if (P.n_peer) __threadfence_system();
+    if (P.mc) asm volatile("fence.proxy.alias;" ::: "memory");
+    if (P.n_peer || P.mc) __threadfence_system();
     if (MODE == MODE_RECUR && P.peaks) {
 #pragma unroll
         for (int k = 0; k < MS; ++k) {

@@ -131,12 +131,14 @@ class DeviceRowEngine:
     """One rank's share of a row-partitioned run on its GPU (C ABI step-wise
     plan over caller-owned torch buffers)."""
 
-    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q, peers=None):
+    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q, peers=None, mc=None):
         from .engine import DeviceMatrix
 
         self.dm = DeviceMatrix(S_local, "float64" if dtype == "f64" else "float32", device)
         self.plan = self.dm.plan(d)
-        if peers is None:
+        if mc is not None:  # fused exchange through NVLS multicast addresses of F[0], F[1]
+            self.plan.partition_multicast(row0, n_global, (F[0].data_ptr(), F[1].data_ptr()), mc)
+        elif peers is None:
             self.plan.partition(row0, n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
         else:  # fused exchange: F = this rank's two full buffers, peers = (parity-0, parity-1) pointer lists
             self.plan.partition_peers(row0, n_global, (F[0].data_ptr(), F[1].data_ptr()), peers[0], peers[1])
@@ -162,24 +164,30 @@ class DeviceRowEngine:
         return out, peaks
 
 
-def peer_buffers(shape, dtype, device, group):
+def peer_buffers(shape, dtype, device, group, multicast: bool = False):
     """Two replicated full buffers in torch symmetric memory (NVLink-mapped on
-    every rank) and, per parity, the device pointers of the peers' copies."""
+    every rank) and, per parity, the device pointers of the peers' copies --
+    or, with multicast=True, the NVLS multicast address of each buffer."""
     import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm_mem
 
     group = dist.group.WORLD if group is None else group
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    F, peers = [], ([], [])
+    F, peers, mc = [], ([], []), []
     for parity in range(2):
         t = symm_mem.empty(*shape, dtype=dtype, device=device)
         t.zero_()
         hdl = symm_mem.rendezvous(t, group)
         F.append(t)
+        if multicast:
+            base = int(hdl.multicast_ptr or 0)  # 0: no multicast object (no NVSwitch / driver support)
+            if not base:
+                raise RuntimeError("NVLS multicast is not available for this group")
+            mc.append(base + (t.data_ptr() - hdl.buffer_ptrs[rank]))
         for p in range(world):
             if p != rank:
                 peers[parity].append(hdl.get_buffer(p, list(shape), dtype).data_ptr())
-    return F, peers
+    return F, (mc if multicast else peers)
 
 
 def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, seed: int = 0,
@@ -199,6 +207,8 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     exchange="peer": the fused exchange -- K1's epilogue stores every Q(r) row
     into all ranks' replicated buffers over NVLink (torch symmetric memory),
     so the transfer overlaps the step; one barrier per step.  GPU only.
+    exchange="multicast": the same through NVLS multicast (one multimem store
+    per row, replicated by the NVSwitch).
     """
     import torch
     import torch.distributed as dist
@@ -217,13 +227,15 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     on_gpu = engine_factory is None
     dev = torch.device(f"cuda:{torch.cuda.current_device() if device is None else device}") if on_gpu \
         else torch.device("cpu")
-    if exchange not in ("allgather", "peer"):
-        raise ValueError("exchange must be 'allgather' or 'peer'")
-    if exchange == "peer":
+    if exchange not in ("allgather", "peer", "multicast"):
+        raise ValueError("exchange must be 'allgather', 'peer' or 'multicast'")
+    if exchange != "allgather":
         if not on_gpu:
             raise ValueError("the fused peer exchange runs on GPUs (torch symmetric memory)")
-        F2, peers = peer_buffers((world * n_pad, ld), tdt, dev, group)
-        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F2, None, peers=peers)
+        mcast = exchange == "multicast"
+        F2, ptrs = peer_buffers((world * n_pad, ld), tdt, dev, group, multicast=mcast)
+        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F2, None,
+                              peers=None if mcast else ptrs, mc=ptrs if mcast else None)
         kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
         eng.begin(coeffs, kind, seed, 0, d)
         flag = torch.zeros(1, device=dev)

@@ -332,6 +332,12 @@ class Plan:
             self.handle, int(row0), int(n_global), C.c_void_p(int(full_ptrs[0])), C.c_void_p(int(full_ptrs[1])),
             n, arr0, arr1), "csemb_plan_partition_peers")
 
+    def partition_multicast(self, row0: int, n_global: int, full_ptrs, mc_ptrs) -> None:
+        """Fused exchange through NVLS multicast addresses of the two full buffers."""
+        _lib.check(self.lib.csemb_plan_partition_multicast(
+            self.handle, int(row0), int(n_global), C.c_void_p(int(full_ptrs[0])), C.c_void_p(int(full_ptrs[1])),
+            C.c_void_p(int(mc_ptrs[0])), C.c_void_p(int(mc_ptrs[1]))), "csemb_plan_partition_multicast")
+
     def begin(self, coeffs, *, block_dev: int | None = None, omega_kind: int = _lib.OMEGA_SPLITMIX, seed: int = 0,
               col0: int = 0, d_global: int | None = None) -> None:
         c = np.ascontiguousarray(coeffs, dtype=np.float64)

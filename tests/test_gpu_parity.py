@@ -579,6 +579,17 @@ class TestRowPartition:
             # the fused exchange through torch symmetric memory (no peers at world 1)
             E2, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="peer")
             assert np.array_equal(E2.cpu().numpy(), ref)
+            # ... and through NVLS multicast, where the node offers it (multimem.st
+            # into the one-replica multicast object)
+            try:
+                E3, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="multicast",
+                                              dtype="f64")
+            except RuntimeError as e:
+                if "multicast is not available" not in str(e):
+                    raise
+                print("NVLS multicast unavailable here:", e)
+            else:
+                assert np.array_equal(E3.cpu().numpy(), ref)
         finally:
             dist.destroy_process_group()
 
