@@ -62,7 +62,8 @@ def kernel_summary(rep, tag, dt):
     lines += ["    " + ln for ln in hot.splitlines()]
     with open(os.path.join(PROF, f"{tag}_k1_{dt}.txt"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    return rd + wr, float(m["gpu__time_duration.sum"][0])
+    return (rd + wr, float(m["gpu__time_duration.sum"][0]), float(m["lts__t_sector_hit_rate.pct"][0]) / 100.0,
+            to_bytes(*m["l1tex__m_xbar2l1tex_read_bytes.sum"]))
 
 
 def launch_summary(path, tag):
@@ -100,9 +101,13 @@ def main(tag):
     for dt in ("f64", "f32"):
         rep = os.path.join(OUT, f"prof_{tag}_k1_{dt}.ncu-rep")
         if os.path.exists(rep):
-            b, ms = kernel_summary(rep, tag, dt)
+            b, ms, hit, xbar = kernel_summary(rep, tag, dt)
             traffic[dt] = int(b)
+            traffic.setdefault("l2_hit_rate", {})[dt] = round(hit, 4)
+            traffic.setdefault("l2_to_sm_bytes", {})[dt] = int(xbar)
     if traffic:
+        traffic["source"] = (f"profiles/{tag}_k1_f64.txt, profiles/{tag}_k1_f32.txt "
+                             "(ncu --set full, one K1 launch, config 2)")
         with open(os.path.join(PROF, "k1_traffic.json"), "w") as fh:
             json.dump(traffic, fh, indent=1)
     ll = os.path.join(OUT, f"launches_{tag}.csv")
