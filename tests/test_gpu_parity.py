@@ -890,3 +890,102 @@ def test_schedule_orders_bit_exact_at_scale(kind, n, d, L, row_order):
     plan.set_load_balance(row_order=0)
     assert np.array_equal(plan.apply(th, 1, om), ref)
     dm.close()
+
+
+# --------------------------------------------------------------------------
+# BASELINE sizes: config 2 in full against the oracle; configs 3 / 4 in full
+# through the fp32 gates against the (bit-exact) fp64 device result
+# --------------------------------------------------------------------------
+def _device_result(plan, d):
+    """E of the plan's last run as an (n, d) torch tensor (device to device)."""
+    import torch
+
+    ptr, ld, dt = plan.output()
+    out = torch.empty((plan.dm.n_rows, d), dtype=torch.float64 if dt == 0 else torch.float32, device="cuda")
+    plan.copy_output_to(out.data_ptr(), d)
+    plan.dm.ctx.sync()
+    return out
+
+
+def _fp32_gates(E32, E64, n, seed):
+    """north_star fp32 gates on device tensors: relative Frobenius error and the
+    row-normalised cosine error on 10^4 sampled row pairs."""
+    import torch
+
+    a, b = E32.double(), E64
+    r = float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+    pairs = torch.from_numpy(O.sample_pairs(n, 10_000, seed)).cuda()
+
+    def cos(X):
+        u, v = X[pairs[:, 0]], X[pairs[:, 1]]
+        den = torch.linalg.norm(u, dim=1) * torch.linalg.norm(v, dim=1)
+        return torch.where(den > 0, (u * v).sum(1) / den, torch.zeros_like(den))
+
+    return r, float((cos(a) - cos(b)).abs().max())
+
+
+def test_config2_full_scale_fp64_bit_exact_and_fp32_gates():
+    # BASELINE configs[1] at its full size and order: SBM n=1e6 (100 blocks,
+    # degree 15 intra + 5 inter), d=80, L=180, f=1{x>=0.95}, the reference's
+    # SplitMix projection (seed 0).  fp64 against the oracle, bit for bit
+    # (~30 s of 16-thread CPU); fp32 through the north_star gates.
+    n, d, L = 1_000_000, 80, 180
+    S = graphs.sbm(n, 100, 15.0, 5.0, seed=2)
+    th = pb.legendre_coefficients(pb.indicator_above(0.95), L).coeffs
+    p64 = pb.DeviceMatrix(S).plan(d)
+    p64.run(th, 1, omega_kind=1, seed=0)
+    E64 = _device_result(p64, d)
+    ref, _, bad = O.run_stage(O.CSR.of(S), th, O.sample_projection(n, d, 0))
+    assert bad == 0
+    assert np.array_equal(E64.cpu().numpy(), ref)
+    del ref
+    p32 = pb.DeviceMatrix(S, "float32").plan(d)
+    p32.run(th, 1, omega_kind=1, seed=0)
+    r, c = _fp32_gates(_device_result(p32, d), E64, n, 3)
+    print(f"config 2 full scale: fp64 bit-exact vs oracle; fp32 rel {r:.3e}, cosine error {c:.3e}")
+    assert r <= FP32_REL and c <= COS_TOL, (r, c)
+
+
+@pytest.mark.parametrize("config", [3, 4])
+def test_configs34_full_scale_fp32_gates(config):
+    # configs 3 / 4 at full size (device-built inputs, as tools/bench_configs.py):
+    # fp32 vs fp64 on identical inputs through the north_star gates; the fp64
+    # path's stored-order arithmetic is pinned bit-exact by the tests above
+    import math
+
+    import torch
+
+    from paper_1509_08360_b200 import device_build as db
+
+    if config == 3:
+        S = db.normalized_adjacency(db.chung_lu_edges(10_000_000, seed=3), 10_000_000)
+        f, d, L = pb.commute_time(0.01), 80, 180
+    else:
+        S = db.dilate(db.bag_of_words(2_000_000, 500_000, seed=4))
+
+        class CutAbove:  # f(x) = x * 1{x >= 0.3} (not a built-in kind)
+            def __call__(self, x):
+                x = np.asarray(x, dtype=np.float64)
+                return np.where(x >= 0.3, x, 0.0)
+
+            def breakpoints(self):
+                return (0.3,)
+
+        f, d, L = pb.odd_extension(CutAbove()), 96, 120
+    torch.cuda.synchronize()
+    th = pb.legendre_coefficients(f, L).coeffs
+    out = {}
+    for dt in ("float64", "float32"):
+        dm = S.to_device_matrix(dt)
+        if config == 4:  # spectrum scaled by the 30-iteration estimate, identical for both dtypes
+            if dt == "float64":
+                est = dm.spectral_norm(30, max(1, math.ceil(6.0 * math.log(S.n_rows))), 11, 1.01)
+            dm.scale(1.0 / est)
+        plan = dm.plan(d)
+        plan.run(th, 1, omega_kind=2, seed=7)
+        out[dt] = _device_result(plan, d)
+        dm.close()
+    assert torch.isfinite(out["float64"]).all()
+    r, c = _fp32_gates(out["float32"], out["float64"], S.n_rows, 5)
+    print(f"config {config} full scale: fp32 rel {r:.3e}, cosine error {c:.3e}")
+    assert r <= FP32_REL and c <= COS_TOL, (r, c)
