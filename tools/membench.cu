@@ -90,6 +90,44 @@ __global__ void k_gather_rows320(const float4 *__restrict__ a, uint32_t nrows, u
     if (acc == 1234.5f) *sink = acc;
 }
 
+// 256-bit loads (sm_100a LDG.E.256): 8 lanes per row of NV 32-byte vectors,
+// lane l reads vectors l, l+8, l+16 (< NV); 640-byte rows: NV = 20, 320-byte: NV = 10
+struct alignas(32) v8f { float v[8]; };
+__device__ __forceinline__ v8f ld256(const v8f *p) {
+    v8f r;
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]), "=f"(r.v[6]),
+                   "=f"(r.v[7]) : "l"(p));
+    return r;
+}
+template <int NV>
+__global__ void k_gather_rows256(const v8f *__restrict__ a, uint32_t nrows, uint32_t iters, float *sink) {
+    constexpr int K = (NV + 7) / 8;
+    const uint32_t lane = threadIdx.x & 7;
+    uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+    uint32_t h = g * 2654435761u + 12345u;
+    float acc = 0.f;
+    for (uint32_t it = 0; it < iters; it += 2) {
+        v8f v[2][K];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            h = h * 1664525u + 1013904223u;
+            const uint32_t row = (uint32_t)(((uint64_t)(h >> 3) * nrows) >> 29);
+            const v8f *p = a + (size_t)row * NV + lane;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (lane + 8 * k < NV) v[u][k] = ld256(p + 8 * k);
+                else v[u][k].v[0] = v[u][k].v[7] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc += v[u][k].v[0] + v[u][k].v[7];
+    }
+    if (acc == 1234.5f) *sink = acc;
+}
+
 template <int CG, int UNROLL>
 __global__ void k_gather(const float4 *__restrict__ a, uint32_t nrows, uint32_t iters, float *sink) {
     const uint32_t lane = threadIdx.x & 7;
@@ -187,6 +225,21 @@ int main() {
         float ms2 = best_ms([&] { k_gather_rows<2, 5><<<grid, block>>>(a, nrows, it2, sink); });
         printf("gather640 %4zu MB: %s %.0f  %s %.0f  %s %.0f GB/s\n", mb, names[0], gb2 / ms0 / 1e6, names[1],
                gb2 / ms1 / 1e6, names[2], gb2 / ms2 / 1e6);
+    }
+    // the same rows through 256-bit loads (8 lanes x 32 B)
+    for (size_t mb : {48, 640, 2048}) {
+        uint32_t nrows = (uint32_t)((mb << 20) / 640);
+        const uint32_t it2 = 64;
+        const double gb2 = (double)lanes_total / 8 * it2 * 640;
+        float ms0 = best_ms([&] { k_gather_rows256<20><<<grid, block>>>((const v8f *)a, nrows, it2, sink); });
+        printf("gather640x256 %4zu MB: nc %.0f GB/s\n", mb, gb2 / ms0 / 1e6);
+    }
+    for (size_t mb : {48, 320, 2048}) {
+        uint32_t nrows = (uint32_t)((mb << 20) / 320);
+        const uint32_t it2 = 64;
+        const double gb2 = (double)lanes_total / 8 * it2 * 320;
+        float ms0 = best_ms([&] { k_gather_rows256<10><<<grid, block>>>((const v8f *)a, nrows, it2, sink); });
+        printf("gather320x256 %4zu MB: nc %.0f GB/s\n", mb, gb2 / ms0 / 1e6);
     }
     // 320-byte rows (f32 d=80, K1's fp32 gather), ld.global.nc
     for (size_t mb : {48, 320, 2048}) {
