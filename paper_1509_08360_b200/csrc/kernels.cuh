@@ -201,6 +201,10 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_BATCH
 #define K1_BATCH 0  // stored entries per warp-uniform batch (<= G; 0: B = G, measured best)
 #endif
+#ifndef K1_EB8
+#define K1_EB8 2  // fp64 entries per lane per batch for 8-lane groups (measured, config 2 graph:
+                  // d=40 f64 0.71 -> 0.67 ms; fp32 8-lane groups and 16-lane groups lose with 2)
+#endif
 #ifndef K1_QSTORE_CS
 #define K1_QSTORE_CS 1  // store Q(r) evict-first (measured: <=1% faster than write-back)
 #endif
@@ -353,15 +357,34 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     if (it < P.n_rows) {
         extent(row_of(it), beg, end);
     }
-    // stored entries advance in batches of B <= G (lanes gl < B hold the batch)
-    constexpr int B = (K1_BATCH > 0 && K1_BATCH < G) ? K1_BATCH : G;
-    static_assert(G % B == 0, "batch width must divide the group width");
-    int myj = 0;
-    T mya = (T)0;
-    if (gl < B && beg + gl < end) {
-        myj = __ldcs(cols + beg + gl);
-        mya = __ldcs(vals + beg + gl);
-    }
+    // Stored entries advance in warp-uniform batches of B.  Narrow groups hold
+    // EB entries per lane (8 / 4 / 2 for 1 / 2 / 4 lanes, 2 for 8 lanes in fp64),
+    // so a batch spans 8-16 entries: the next batch's column ids and values are loaded that
+    // many steps before use (with one entry per lane, a 1-lane group would wait
+    // on an index load at every entry).  Entry t of a
+    // batch sits in lane t % G, slot t / G; wide groups keep B = G (or K1_BATCH).
+    constexpr int EB = G == 1 ? 8 : G == 2 ? 4 : G == 4 ? 2 : G == 8 ? (sizeof(T) == 8 ? K1_EB8 : 1) : 1;
+    constexpr int B = EB > 1 ? G * EB : ((K1_BATCH > 0 && K1_BATCH < G) ? K1_BATCH : G);
+    static_assert(EB > 1 || G % B == 0, "batch width must divide the group width");
+    constexpr int BL = EB > 1 ? G : B;  // lanes that hold the batch
+    auto load_batch = [&](int64_t b0, int64_t e0, int (&j)[EB], T (&a)[EB]) {
+#pragma unroll
+        for (int k = 0; k < EB; ++k) {
+            j[k] = 0;
+            a[k] = (T)0;
+            const int64_t q = b0 + gl + k * G;
+            if (gl < BL && q < e0) {
+                j[k] = __ldcs(cols + q);
+                a[k] = __ldcs(vals + q);
+            }
+        }
+    };
+    // entry t (compile-time) of a batch held in (j or a)[EB], broadcast to the group
+    auto bcast_j = [&](const int (&j)[EB], int t) { return __shfl_sync(0xFFFFFFFFu, j[t / G], t % G, G); };
+    auto bcast_a = [&](const T (&a)[EB], int t) { return __shfl_sync(0xFFFFFFFFu, a[t / G], t % G, G); };
+    int myj[EB];
+    T mya[EB];
+    load_batch(beg, end, myj, mya);
 
     // Gathers of the first D-1 entries of the current batch are carried across
     // batches.  Register variant: D-deep rotating register buffer.  Staged
@@ -416,7 +439,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         }
     };
 #pragma unroll
-    for (int e = 0; e < D - 1; ++e) issue(e, __shfl_sync(0xFFFFFFFFu, myj, e, G), e < end - beg);
+    for (int e = 0; e < D - 1; ++e) issue(e, bcast_j(myj, e), e < end - beg);
 
     for (int64_t wbase = warp * RPW; wbase < P.n_rows; wbase += wstride) {  // warp-uniform
         const bool active = it < P.n_rows;
@@ -454,20 +477,20 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
 
         for (int b = 0; b < nb; ++b) {
             // prefetch the next batch of this row, else the next row's first batch
-            int nj = 0;
-            T na = (T)0;
+            int nj[EB];
+            T na[EB];
             int ncnt = 0;  // entries of that next batch for my row
             if (b + 1 < nb_mine) {
                 ncnt = len - (b + 1) * B;
-                if (gl < B && beg + (b + 1) * B + gl < end) {
-                    nj = __ldcs(cols + beg + (b + 1) * B + gl);
-                    na = __ldcs(vals + beg + (b + 1) * B + gl);
-                }
+                load_batch(beg + (b + 1) * B, end, nj, na);
             } else if (b + 1 >= nb) {
                 ncnt = (int)(end2 - beg2);
-                if (gl < B && beg2 + gl < end2) {
-                    nj = __ldcs(cols + beg2 + gl);
-                    na = __ldcs(vals + beg2 + gl);
+                load_batch(beg2, end2, nj, na);
+            } else {
+#pragma unroll
+                for (int k = 0; k < EB; ++k) {
+                    nj[k] = 0;
+                    na[k] = (T)0;
                 }
             }
             const int cnt = len - b * B;  // entries of this batch for my row (may be <= 0)
@@ -481,17 +504,16 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 // lanes gl < pf_lines each request one 128-byte line of that row, so the
                 // register gather D steps ahead finds it in L2
                 if constexpr (STAGED == 0) {
-                    const int jn = __shfl_sync(0xFFFFFFFFu, nj, t, G);
+                    const int jn = bcast_j(nj, t);
                     if (gl < pf_lines && t < ncnt)
                         prefetch_l2(reinterpret_cast<const char *>(ycur - gl + (int64_t)jn * P.ldv) + gl * 128);
                 }
 #endif
                 const int e = t + D - 1;
-                const int j = (e < B) ? __shfl_sync(0xFFFFFFFFu, myj, e % B, G)
-                                      : __shfl_sync(0xFFFFFFFFu, nj, e % B, G);
+                const int j = (e < B) ? bcast_j(myj, e % B) : bcast_j(nj, e % B);
                 const bool more = (e < B) ? (e < cnt) : (e - B < ncnt);
                 if (D > 1) issue(e % D, j, more);
-                const T a = __shfl_sync(0xFFFFFFFFu, mya, t, G);
+                const T a = bcast_a(mya, t);
                 if (D == 1) issue(0, j, more);
                 if constexpr (STAGED == 2) {
                     cp_async_wait<D - 1>();  // entry t has landed (this lane's own copies)
@@ -520,19 +542,17 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 }
             }
             if (b + 1 < nb_mine || b + 1 >= nb) {
-                myj = nj;
-                mya = na;
+#pragma unroll
+                for (int k = 0; k < EB; ++k) {
+                    myj[k] = nj[k];
+                    mya[k] = na[k];
+                }
             }
         }
         if (nb == 0) {  // every row of the warp is empty: move to the next rows' first batch
-            myj = 0;
-            mya = (T)0;
-            if (gl < B && beg2 + gl < end2) {
-                myj = __ldcs(cols + beg2 + gl);
-                mya = __ldcs(vals + beg2 + gl);
-            }
+            load_batch(beg2, end2, myj, mya);
 #pragma unroll
-            for (int e = 0; e < D - 1; ++e) issue(e, __shfl_sync(0xFFFFFFFFu, myj, e, G), e < end2 - beg2);
+            for (int e = 0; e < D - 1; ++e) issue(e, bcast_j(myj, e), e < end2 - beg2);
         }
 
         if (active) {
