@@ -28,19 +28,33 @@ ap.add_argument("--dtype", default="f64,f32")
 ap.add_argument("--L", type=int, default=20)
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--d", type=int, default=80)
+ap.add_argument("--config", type=int, default=2, help="2: SBM (host-built); 3 / 4: full-scale device-built inputs")
 args = ap.parse_args()
 warnings.filterwarnings("ignore", message="Sparse CSR tensor support is in beta")
 
-S = graphs.sbm(args.n, 100, 15.0, 5.0, seed=2)
-coeffs = pb.legendre_coefficients(pb.indicator_above(0.95), args.L).coeffs
 dev = torch.device("cuda:0")
+if args.config == 2:
+    S = graphs.sbm(args.n, 100, 15.0, 5.0, seed=2)
+    crow, col = torch.from_numpy(S.row_offsets), torch.from_numpy(S.col_indices)
+    val = torch.from_numpy(S.values)
+else:
+    from paper_1509_08360_b200 import device_build as db
+
+    if args.config == 3:
+        S = db.normalized_adjacency(db.chung_lu_edges(10_000_000, seed=3), 10_000_000)
+    else:
+        S = db.dilate(db.bag_of_words(2_000_000, 500_000, seed=4))
+        S.values.mul_(1.0 / 130.35983614177252)  # the 30-iteration norm estimate (profiles/r1_configs34.json)
+        args.d = 96
+    crow, col, val = S.row_offsets, S.col_indices, S.values
+    args.n = S.n_rows
+coeffs = pb.legendre_coefficients(pb.indicator_above(0.95), args.L).coeffs
 out = []
 for dt in args.dtype.split(","):
     tdt = torch.float64 if dt == "f64" else torch.float32
     # int32 offsets and column ids (the narrower cuSPARSE index type, like K1's int32 columns)
-    A = torch.sparse_csr_tensor(torch.from_numpy(S.row_offsets).to(dev, torch.int32),
-                                torch.from_numpy(S.col_indices).to(dev, torch.int32),
-                                torch.from_numpy(S.values).to(dev, tdt), size=(S.n_rows, S.n_cols))
+    A = torch.sparse_csr_tensor(crow.to(dev, torch.int32), col.to(dev, torch.int32), val.to(dev, tdt),
+                                size=(S.n_rows, S.n_cols))
     q_prev = torch.randn(args.n, args.d, device=dev, dtype=tdt)
     q_prev2 = torch.randn(args.n, args.d, device=dev, dtype=tdt)
     E = torch.zeros(args.n, args.d, device=dev, dtype=tdt)
@@ -70,7 +84,8 @@ for dt in args.dtype.split(","):
     torch.cuda.synchronize()
     spmm_ms = sp[0].elapsed_time(sp[1])
     # the fused K1 on the same graph
-    dm = pb.DeviceMatrix(S, "float64" if dt == "f64" else "float32")
+    dm = pb.DeviceMatrix(S, "float64" if dt == "f64" else "float32") if args.config == 2 else \
+        S.to_device_matrix("float64" if dt == "f64" else "float32")
     plan = dm.plan(args.d)
     for _ in range(2):
         plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
@@ -78,7 +93,7 @@ for dt in args.dtype.split(","):
     _, k1_tot, launches = plan.timing()
     k1_ms = k1_tot / args.L
     dm.close()
-    line = {"dtype": dt, "n": args.n, "nnz": S.nnz, "d": args.d, "cusparse_step_ms": round(base_ms, 4),
+    line = {"config": args.config, "dtype": dt, "n": args.n, "nnz": S.nnz, "d": args.d, "cusparse_step_ms": round(base_ms, 4),
             "cusparse_spmm_ms": round(spmm_ms, 4), "fused_k1_ms": round(k1_ms, 4),
             "fused_speedup": round(base_ms / k1_ms, 2)}
     print(json.dumps(line), flush=True)
