@@ -192,7 +192,8 @@ def peer_buffers(shape, dtype, device, group, multicast: bool = False):
 
 def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, seed: int = 0,
                           omega_kind: str = "reference", dtype: str = "f64", normalize_rows: bool = False,
-                          group=None, device: int | None = None, engine_factory=None, exchange: str = "allgather"):
+                          group=None, device: int | None = None, engine_factory=None, exchange: str = "allgather",
+                          col0: int = 0, d_global: int | None = None):
     """E rows [row0, row0 + n_local) of f_L(S) Omega for a row-partitioned S.
 
     Each rank holds its row block of S (global column ids); every step gathers
@@ -209,6 +210,8 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     so the transfer overlaps the step; one barrier per step.  GPU only.
     exchange="multicast": the same through NVLS multicast (one multimem store
     per row, replicated by the NVSwitch).
+    col0 / d_global: the d columns are the slice [col0, col0 + d) of a
+    d_global-column projection (the 2-D layout, `embed_2d`).
     """
     import torch
     import torch.distributed as dist
@@ -237,7 +240,7 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
         eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F2, None,
                               peers=None if mcast else ptrs, mc=ptrs if mcast else None)
         kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
-        eng.begin(coeffs, kind, seed, 0, d)
+        eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
         flag = torch.zeros(1, device=dev)
         for r in range(1, len(coeffs)):
             eng.step(r)  # host-synchronous: this rank's stores of Q(r) are complete
@@ -253,7 +256,7 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     else:
         eng = engine_factory(S_local, row0, n_global, d, dtype, F, q)
     kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
-    eng.begin(coeffs, kind, seed, 0, d)
+    eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
     order = len(coeffs) - 1
     parts = [F[p * n_pad:(p + 1) * n_pad] for p in range(world)]
     for r in range(1, order + 1):
@@ -265,3 +268,67 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
                 dist.all_gather(parts, q[r & 1], group=group)
     E, peaks = eng.end(normalize_rows)
     return E, combine_peaks(peaks, group)
+
+
+# ---------------------------------------------------------------------------
+# 2-D layout: row blocks x column shards
+# ---------------------------------------------------------------------------
+def grid_groups(R: int, C: int):
+    """Sub-groups of an R x C rank grid (rank = rr * C + cc): for every column
+    shard cc the R ranks that exchange Q(r) each step, for every row block rr
+    the C ranks that assemble its columns at the end.  Collective: every rank
+    creates every group, in the same order."""
+    import torch.distributed as dist
+
+    if R * C != dist.get_world_size():
+        raise ValueError(f"grid {R} x {C} does not match world size {dist.get_world_size()}")
+    row_groups = [dist.new_group([rr * C + cc for rr in range(R)]) for cc in range(C)]
+    col_groups = [dist.new_group([rr * C + cc for cc in range(C)]) for rr in range(R)]
+    return row_groups, col_groups
+
+
+def embed_2d(S, coeffs, d: int, grid: tuple[int, int], *, seed: int = 0, omega_kind: str = "reference",
+             dtype: str = "f64", normalize_rows: bool = True, device: int | None = None, engine_factory=None,
+             exchange: str = "allgather", groups=None):
+    """E rows of this rank's row block (all d columns) on an R x C rank grid.
+
+    Column sharding replicates the whole matrix and leaves every rank the full
+    per-row work on d/N columns; the row partition exchanges all of Q(r) every
+    step.  The grid trades the two: rank (rr, cc) holds row block rr of S
+    (global column ids) and runs the row-partitioned recurrence on column
+    shard cc with the R ranks of its shard (one exchange of Q(r) per step, R x
+    smaller than the 1-D row partition's), then the C ranks of its row block
+    all-gather their column slices and K4 normalises the assembled rows.
+    Every element is computed exactly as on one GPU: bit-identical results.
+    `groups` = grid_groups(R, C) (create them once and reuse)."""
+    import torch
+    import torch.distributed as dist
+
+    R, C = grid
+    rank = dist.get_rank()
+    rr, cc = divmod(rank, C)
+    row_groups, col_groups = groups if groups is not None else grid_groups(R, C)
+    _, blocks = row_blocks(S.n_rows, R)
+    lo_r, hi_r = blocks[rr]
+    align = 2 if dtype == "f64" else 4
+    lo_c, hi_c = column_shards(d, C, align)[cc]
+    S_local = local_rows(S, lo_r, hi_r)
+    E_local, peaks = embed_row_partitioned(
+        S_local, lo_r, S.n_rows, coeffs, hi_c - lo_c, seed=seed, omega_kind=omega_kind, dtype=dtype,
+        normalize_rows=False, group=row_groups[cc], device=device, engine_factory=engine_factory,
+        exchange=exchange, col0=lo_c, d_global=d)
+    E = assemble_columns(E_local, C, d, dtype, group=col_groups[rr])
+    if normalize_rows and E.shape[0] > 0:
+        if E.is_cuda:
+            from . import _lib
+
+            ctx = _lib.context(E.device.index)
+            torch.cuda.synchronize(E.device)
+            _lib.check(ctx.lib.csemb_rownorm(ctx.handle, E.data_ptr(), E.shape[0], d, d,
+                                             _lib.F64 if dtype == "f64" else _lib.F32), "csemb_rownorm")
+            ctx.sync()
+        else:  # CPU tests (oracle engine): the reference cosine harness's normalisation
+            nrm = torch.linalg.norm(E, dim=1, keepdim=True)
+            E = torch.where(nrm > 0, E / torch.where(nrm > 0, nrm, torch.ones_like(nrm)), torch.zeros_like(E))
+    return E, combine_peaks(peaks, col_groups[rr])
+

@@ -120,7 +120,7 @@ class OracleRowEngine:
     def begin(self, coeffs, kind, seed, col0, d_global):
         assert kind == 1  # reference hash
         self.coeffs = coeffs
-        full = O.sample_projection(self.N, d_global, seed)
+        full = O.sample_projection(self.N, d_global, seed, col0, self.d)  # columns [col0, col0 + d)
         self.F[:self.N, :self.d] = torch.from_numpy(full)
         q0 = full[self.row0:self.row0 + self.n]
         self.q[0][:self.n, :self.d] = torch.from_numpy(q0)
@@ -212,3 +212,70 @@ def test_row_partitioned_exchange_argument(tmp_path):
     for p in range(2):
         msgs = open(out + f".{p}.txt").read().split("\n")
         assert "GPUs" in msgs[0] and "exchange must be" in msgs[1]
+
+
+# ---------------------------------------------------------------------------
+# 2-D layout (row blocks x column shards), oracle engine on CPU
+# ---------------------------------------------------------------------------
+def _grid_worker(rank, world, port, grid, d, seed, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import embed_2d, grid_groups
+
+        S, coeffs = _problem()
+        groups = grid_groups(*grid)
+        E, peaks = embed_2d(_as_sparse(S), coeffs, d, grid, seed=seed, engine_factory=OracleRowEngine,
+                            normalize_rows=False, groups=groups)
+        np.save(result_path + f".{rank}.npy", E.numpy())
+        En, _ = embed_2d(_as_sparse(S), coeffs, d, grid, seed=seed, engine_factory=OracleRowEngine, groups=groups)
+        np.save(result_path + f".{rank}.norm.npy", En.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (1, 2), (2, 1)])
+def test_2d_grid_matches_single_process(tmp_path, grid):
+    from paper_1509_08360_b200.distributed import row_blocks
+
+    d, seed = 37, 5
+    world = grid[0] * grid[1]
+    out = str(tmp_path / "grid")
+    mp.start_processes(_grid_worker, args=(world, _free_port(), grid, d, seed, out), nprocs=world,
+                       start_method="spawn", join=True)
+    S, coeffs = _problem()
+    ref, _, _ = O.run_stage(S, coeffs, O.sample_projection(S.n_rows, d, seed))
+    _, blocks = row_blocks(S.n_rows, grid[0])
+    for rank in range(world):
+        lo, hi = blocks[rank // grid[1]]
+        assert np.array_equal(np.load(out + f".{rank}.npy"), ref[lo:hi])  # every rank: its rows, all columns
+        np.testing.assert_allclose(np.load(out + f".{rank}.norm.npy"), O.row_normalize(ref)[lo:hi], rtol=0,
+                                   atol=1e-15)
+
+
+def test_grid_shape_must_match_world(tmp_path):
+    out = str(tmp_path / "bad")
+
+    mp.start_processes(_bad_grid_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn", join=True)
+    for p in range(2):
+        assert "does not match world size" in open(out + f".{p}.txt").read()
+
+
+def _bad_grid_worker(rank, world, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import grid_groups
+
+        try:
+            grid_groups(2, 2)
+            msg = "no error"
+        except ValueError as e:
+            msg = str(e)
+        with open(result_path + f".{rank}.txt", "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()
+

@@ -579,6 +579,14 @@ class TestRowPartition:
             # the fused exchange through torch symmetric memory (no peers at world 1)
             E2, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="peer")
             assert np.array_equal(E2.cpu().numpy(), ref)
+            # the 2-D grid driver at 1 x 1 (row partition + column assembly + K4), both exchanges
+            from paper_1509_08360_b200.distributed import embed_2d
+
+            for ex in ("allgather", "peer"):
+                E4, _ = embed_2d(S, th, 24, (1, 1), seed=2, device=0, exchange=ex, normalize_rows=False)
+                assert np.array_equal(E4.cpu().numpy(), ref), ex
+            E5, _ = embed_2d(S, th, 24, (1, 1), seed=2, device=0)
+            np.testing.assert_allclose(E5.cpu().numpy(), O.row_normalize(ref), rtol=0, atol=1e-15)
             # ... and through NVLS multicast, where the node offers it (multimem.st
             # into the one-replica multicast object)
             try:
