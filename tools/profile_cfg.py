@@ -25,6 +25,7 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--dtype", default="f32")
 ap.add_argument("--L", type=int, default=3)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--split", default=None, help="comma list of split thresholds to run in turn (0 = never split)")
 args = ap.parse_args()
 
 if args.config == 3:
@@ -39,10 +40,13 @@ if scale != 1.0:
     dm.scale(scale)
 coeffs = pb.legendre_coefficients(f, args.L).coeffs
 plan = dm.plan(d)
-for _ in range(args.reps):
-    plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
-    dm.ctx.sync()
-    tot, steps, launches = plan.timing()
-    print(f"config {args.config} {args.dtype}: K1 {steps / args.L:.3f} ms/step ({launches // args.L} launches/step)",
-          flush=True)
+for thr in ([None] if args.split is None else [int(x) for x in args.split.split(",")]):
+    if thr is not None:
+        plan.set_load_balance(split_threshold=thr)
+    for _ in range(args.reps):
+        plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7)
+        dm.ctx.sync()
+        tot, steps, launches = plan.timing()
+        print(f"config {args.config} {args.dtype} split={thr}: K1 {steps / args.L:.3f} ms/step "
+              f"({launches // args.L} launches/step)", flush=True)
 dm.close()
