@@ -105,7 +105,7 @@ int csemb_plan_destroy(csemb_plan *p);
  *    reference's stored-order accumulation (bit-exact).  */
 #define CSEMB_OPT_EXACT_PEAKS 1
 #define CSEMB_OPT_REVERSE_SWEEP 2
-#define CSEMB_OPT_SPLIT_THRESHOLD 3 /* rows longer than this (default 4096) are split
+#define CSEMB_OPT_SPLIT_THRESHOLD 3 /* rows longer than this (default 2048) are split
                                        into 1024-entry chunks summed in chunk order;
                                        0 = never split (bit-exact for every input) */
 #define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default: 1 for skewed row lengths,

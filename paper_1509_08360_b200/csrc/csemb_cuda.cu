@@ -35,6 +35,11 @@ int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+// Rows longer than this are split into HEAVY_CHUNK-entry chunks (K1a / K1c).
+// Measured on the skewed configs (fp32 K1 per step): 4096 -> 2048 is -2.5%
+// (config 4) and -2.9% (config 3); 8192 / 16384 are 5-17% slower.
+static const int64_t DEFAULT_SPLIT = 2048;
+
 struct csemb_plan {
     csemb_mat *m = nullptr;
     int64_t d = 0, ld = 0;  // ld in elements
@@ -52,7 +57,7 @@ struct csemb_plan {
     // options (csemb_plan_set_option)
     int exact_peaks = 0;
     int reverse_sweep = 1;
-    int64_t split_threshold = 4096;  // 0: never split rows (bit-exact for every input)
+    int64_t split_threshold = DEFAULT_SPLIT;  // 0: never split rows (bit-exact for every input)
     int e_fold = 3;                  // E read/written every e_fold steps (1..3), same roundings
     int row_order = -1;              // -1 auto, 0 natural, 1 bucketed, 2 windowed (auto window), >= 64 window
     void *partials = nullptr;        // heavy-row chunk partial sums
@@ -1513,7 +1518,7 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     Schedule *sc = nullptr;
     void *partials = nullptr;
     if (e == cudaSuccess) {
-        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), 4096, -1, &sc);
+        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), DEFAULT_SPLIT, -1, &sc);
         if (rc) {
             dfree(c, V); dfree(c, Wm); dfree(c, stage); dfree(c, partial); dfree(c, rq); dfree(c, inv);
             return rc;

@@ -246,7 +246,7 @@ class Plan:
         _lib.check(self.lib.csemb_plan_set_option(self.handle, int(option), int(value)), "csemb_plan_set_option")
 
     def set_load_balance(self, split_threshold: int | None = None, row_order: int | None = None) -> None:
-        """Rows longer than split_threshold (default 4096; 0 = never) are split
+        """Rows longer than split_threshold (default 2048; 0 = never) are split
         into chunks summed in chunk order (no longer bit-identical to the
         reference's sequential sum for those rows); row_order -1 auto /
         0 natural / 1 bucketed by length / 2 bucketed within windows of
