@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace csemb {
 
 enum { MODE_RECUR = 0, MODE_SPMM = 1 };
@@ -201,6 +203,12 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_BATCH
 #define K1_BATCH 0  // stored entries per warp-uniform batch (<= G; 0: B = G, measured best)
 #endif
+#ifndef K1_TRIM
+#define K1_TRIM 0  // 1: trim the warp's last batch to its longest row (rounded up to D)
+#endif
+#ifndef K1_EB8F32
+#define K1_EB8F32 1  // fp32 entries per lane per batch for 8-lane groups
+#endif
 #ifndef K1_EB8
 #define K1_EB8 2  // fp64 entries per lane per batch for 8-lane groups (measured, config 2 graph:
                   // d=40 f64 0.71 -> 0.67 ms; fp32 8-lane groups and 16-lane groups lose with 2)
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     // many steps before use (with one entry per lane, a 1-lane group would wait
     // on an index load at every entry).  Entry t of a
     // batch sits in lane t % G, slot t / G; wide groups keep B = G (or K1_BATCH).
-    constexpr int EB = G == 1 ? 8 : G == 2 ? 4 : G == 4 ? 2 : G == 8 ? (sizeof(T) == 8 ? K1_EB8 : 1) : 1;
+    constexpr int EB = G == 1 ? 8 : G == 2 ? 4 : G == 4 ? 2 : G == 8 ? (sizeof(T) == 8 ? K1_EB8 : K1_EB8F32) : 1;
     constexpr int B = EB > 1 ? G * EB : ((K1_BATCH > 0 && K1_BATCH < G) ? K1_BATCH : G);
     static_assert(EB > 1 || G % B == 0, "batch width must divide the group width");
     constexpr int BL = EB > 1 ? G : B;  // lanes that hold the batch
@@ -451,7 +459,13 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         }
         const int len = (int)(end - beg);
         const int nb_mine = (len + B - 1) / B;
-        const int nb = __reduce_max_sync(0xFFFFFFFFu, (unsigned)nb_mine);
+        // the warp's batch count, from its longest row (needed by K1_TRIM) or from
+        // the rows' batch counts -- the same number; the choice only moves code
+        // generation, and was measured: from the length, fp32 K1 is 5% faster on
+        // config 4 and 1.4% on config 3, fp64 1.3% slower on config 2
+        constexpr bool NB_FROM_LEN = K1_TRIM || sizeof(T) == 4;
+        const int smax = NB_FROM_LEN ? (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)len) : 0;
+        const int nb = NB_FROM_LEN ? (smax + B - 1) / B : (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)nb_mine);
 #if K1_PREFETCH
         // the epilogue's streamed rows (Q(r-2), E, own Q(r-1)) are requested into
         // L2 now, so the loads after the gather loop hit L2 instead of DRAM
@@ -496,9 +510,15 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             const int cnt = len - b * B;  // entries of this batch for my row (may be <= 0)
             // branch-free pipeline, D entries deep: step t issues entry t+D-1
             // (spilling into the NEXT batch's first entries near the end, so no
-            // batch or row-set epilogue starts with an empty pipeline) and consumes t
-#pragma unroll
-            for (int t = 0; t < B; ++t) {
+            // batch or row-set epilogue starts with an empty pipeline) and consumes t.
+            // K1_TRIM: the warp's last batch runs only its longest row's remaining
+            // entries rounded up to D (a multiple of D keeps slot = step % D); the
+            // entries it spills into the next batch are then the first D-1 <= G,
+            // all in register slot 0 of their lanes.
+            constexpr bool TRIM = K1_TRIM && STAGED == 0 && D - 1 <= G;
+            const int nst = (TRIM && b + 1 == nb) ? min(B, (smax - b * B + D - 1) / D * D) : B;
+            auto step = [&](const int t, const int ns, auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
 #if K1_GATHER_PF
                 // L2 prefetch of entry t of the NEXT batch (B steps ahead, no registers):
                 // lanes gl < pf_lines each request one 128-byte line of that row, so the
@@ -510,8 +530,17 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 }
 #endif
                 const int e = t + D - 1;
-                const int j = (e < B) ? bcast_j(myj, e % B) : bcast_j(nj, e % B);
-                const bool more = (e < B) ? (e < cnt) : (e - B < ncnt);
+                int j;
+                bool more;
+                if constexpr (FULL) {
+                    j = (e < B) ? bcast_j(myj, e % B) : bcast_j(nj, e % B);
+                    more = (e < B) ? (e < cnt) : (e - B < ncnt);
+                } else {
+                    const bool cur = e < ns;
+                    const int src = cur ? myj[(e < B ? e : 0) / G] : nj[0];
+                    j = __shfl_sync(0xFFFFFFFFu, src, cur ? e % G : e - ns, G);
+                    more = cur ? (e < cnt) : (e - ns < ncnt);
+                }
                 if (D > 1) issue(e % D, j, more);
                 const T a = bcast_a(mya, t);
                 if (D == 1) issue(0, j, more);
@@ -539,6 +568,16 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                     // exactly, because acc is never -0 (it starts at +0, as scipy's y does)
 #pragma unroll
                     for (int k = 0; k < VPL; ++k) acc[k] = vmadd(acc[k], a, buf[t % D][k]);
+                }
+            };
+            if (nst == B) {
+#pragma unroll
+                for (int t = 0; t < B; ++t) step(t, B, std::true_type{});
+            } else {
+#pragma unroll
+                for (int t = 0; t < B; ++t) {
+                    if (t % D == 0 && t >= nst) break;  // warp-uniform
+                    step(t, nst, std::false_type{});
                 }
             }
             if (b + 1 < nb_mine || b + 1 >= nb) {
