@@ -429,10 +429,69 @@ def _log_steps(peaks: np.ndarray, d: int, col_base: int = 0) -> None:
                              float(peaks[st, r - 1, ch]))
 
 
+def _run_devices(S, coeffs, n_stages, block, devices, *, dtype, normalize_rows, omega_kind, seed, d):
+    """One process, several GPUs: the d columns are independent (Theorem 1,
+    PAPER.md:100), so each device runs its column shard concurrently (the
+    ctypes calls release the GIL) with the projection hashed on global
+    columns; the shards are assembled on the host and, if asked, row-
+    normalised by K4 on the first device.  Bit-identical to one device."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .distributed import column_shards
+
+    width = 4 if dtype_code(dtype) == _lib.F32 else 2
+    shards = [(dev, lo, hi) for dev, (lo, hi) in zip(devices, column_shards(d, len(devices), width)) if hi > lo]
+    debug = logger.isEnabledFor(logging.DEBUG)
+
+    def one(item):
+        dev, lo, hi = item
+        plan = device_matrix(S, dtype, dev).plan(hi - lo)
+        plan.set_exact_peaks(debug)
+        blk = None if block is None else np.ascontiguousarray(block[:, lo:hi])
+        try:
+            out = plan.apply(coeffs, n_stages, blk, omega_kind=omega_kind, seed=seed, col0=lo, d_global=d)
+            return out, plan.peaks, None
+        except DivergenceError as e:
+            return None, None, e
+
+    with ThreadPoolExecutor(len(shards)) as pool:
+        results = list(pool.map(one, shards))
+    bad = [e for _, _, e in results if e is not None]
+    if bad:  # the first non-finite step over all columns, as the reference reports it
+        import re
+
+        raise min(bad, key=lambda e: int(re.search(r"r=(\d+)", str(e)).group(1)))
+    out = np.empty((S.n_rows, d), dtype=np.float64)
+    for (dev, lo, hi), (part, _, _) in zip(shards, results):
+        out[:, lo:hi] = part
+    if debug:  # per-chunk maxima: each shard reports its global chunks, max-combined (NaN keys dominate)
+        keys = np.maximum.reduce([np.ascontiguousarray(pk).view(np.uint64) for _, pk, _ in results])
+        _log_steps(keys.view(np.float64), d)
+    if normalize_rows:
+        ctx = _lib.context(devices[0])
+        import torch
+
+        E = torch.from_numpy(out).to(f"cuda:{devices[0]}")
+        torch.cuda.synchronize(E.device)
+        _lib.check(ctx.lib.csemb_rownorm(ctx.handle, E.data_ptr(), S.n_rows, d, d, _lib.F64), "csemb_rownorm")
+        ctx.sync()
+        out = E.cpu().numpy()
+    return out
+
+
 def _run(S, coeffs, n_stages, block, *, dtype, device, normalize_rows, omega_kind=_lib.OMEGA_GIVEN,
          seed=0, d=None):
     if S.n_rows != S.n_cols:
         raise ValueError("the recurrence requires a square (symmetric) matrix")
+    if isinstance(device, (list, tuple)):  # devices=[...]: column shards over several GPUs
+        devices = [int(x) for x in device]
+        if not devices:
+            raise ValueError("device list must not be empty")
+        if len(devices) > 1:
+            return _run_devices(S, coeffs, n_stages, block, devices, dtype=dtype, normalize_rows=normalize_rows,
+                                omega_kind=omega_kind, seed=seed,
+                                d=block.shape[1] if block is not None else int(d))
+        device = devices[0]
     dm = device_matrix(S, dtype, device)
     d = block.shape[1] if block is not None else int(d)
     plan = dm.plan(d)
@@ -483,7 +542,9 @@ def fast_embed_cascaded(S, f, cfg: EmbedConfig, omega=None, *, quadrature=None, 
     """b cascade stages of order L/b on the b-th root of f (engine.py:302-349).
 
     With omega=None the projection is generated on the device (the reference's
-    SplitMix64 hash, bit-identical, or Philox with omega_kind="philox")."""
+    SplitMix64 hash, bit-identical, or Philox with omega_kind="philox").
+    device may be a list of GPUs: the columns are sharded across them in one
+    process (bit-identical to one GPU; every entry point accepts this)."""
     if S.n_rows != S.n_cols:
         raise ValueError("fast_embed_cascaded requires a square (symmetric) matrix")
     kind = _lib.OMEGA_GIVEN

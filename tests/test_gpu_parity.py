@@ -446,6 +446,41 @@ class TestDeviceBuild:
 # --------------------------------------------------------------------------
 # row partition (config 5 layout): emulated ranks on one GPU, NCCL driver at ws=1
 # --------------------------------------------------------------------------
+def test_device_list_column_shards_bit_exact(config1, caplog):
+    # device=[0, 0]: two column shards driven concurrently from one process
+    # (both on the one GPU here), assembled, optionally K4-normalised
+    z, meta = config1
+    S = sparse_from(z)
+    cfg = pb.EmbedConfig(L=60, d=40, seed=0)
+    one = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), cfg).values
+    two = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), cfg, device=[0, 0]).values
+    assert np.array_equal(one, two)
+    assert sha(two) == meta["E_sha256"]
+    three = pb.fast_embed_cascaded(S, pb.indicator_above(0.9), cfg, device=[0, 0, 0], normalize_rows=True).values
+    assert np.array_equal(three, pb.fast_embed_cascaded(S, pb.indicator_above(0.9), cfg, normalize_rows=True).values)
+    om = O.sample_projection(2000, 40, 3)
+    th = pb.legendre_coefficients(pb.indicator_above(0.9), 12)
+    a = pb.fast_embed_eig(S, th, 12, om, dtype="float32", device=[0, 0]).values
+    assert np.array_equal(a, pb.fast_embed_eig(S, th, 12, om, dtype="float32").values)
+    # the debug log equals the one-device log (chunk maxima combined over shards)
+    with caplog.at_level(logging.DEBUG, logger="csemb.engine"):
+        pb.fast_embed_eig(S, th, 12, om, device=[0, 0])
+    multi = [r.getMessage() for r in caplog.records if r.getMessage().startswith("stage=")]
+    caplog.clear()
+    with caplog.at_level(logging.DEBUG, logger="csemb.engine"):
+        pb.fast_embed_eig(S, th, 12, om)
+    single = [r.getMessage() for r in caplog.records if r.getMessage().startswith("stage=")]
+    assert multi == single and len(single) == 24
+    # divergence: the first bad step over all shards
+    with pytest.raises(pb.DivergenceError) as e1:
+        pb.fast_embed_eig(pb.scale_values(S, 1e40), th, 12, om, device=[0, 0])
+    with pytest.raises(pb.DivergenceError) as e2:
+        pb.fast_embed_eig(pb.scale_values(S, 1e40), th, 12, om)
+    assert str(e1.value) == str(e2.value)
+    with pytest.raises(ValueError):
+        pb.fast_embed_eig(S, th, 12, om, device=[])
+
+
 class TestRowPartition:
     @pytest.mark.parametrize("dtype", ["float64", "float32"])
     def test_emulated_ranks_bit_exact(self, dtype):
