@@ -15,6 +15,8 @@ Shard boundaries are multiples of the 16-byte vector width (2 columns in f64,
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 
@@ -65,6 +67,52 @@ def combine_peaks(peaks: np.ndarray, group=None) -> np.ndarray:
     return keys.cpu().numpy().view(np.float64).reshape(peaks.shape)
 
 
+def broadcast_matrix(S, src: int = 0, group=None, device: int | None = None):
+    """C1: replicate rank `src`'s CSR on every rank of `group`.
+
+    Only `src` needs S (other ranks pass None).  The offsets (int64), column
+    ids (int32) and values (f64) travel as three broadcasts: NCCL over NVLink
+    for GPU tensors, landing directly in device memory as a DeviceCSR (upload
+    with `.to_device_matrix`, no host copy); gloo on CPU returns a host
+    SparseMatrix.  Values are bit-identical on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    from .sparse import SparseMatrix
+
+    rank = dist.get_rank(group)
+    on_gpu = dist.get_backend(group) == "nccl"
+    dev = torch.device(f"cuda:{torch.cuda.current_device() if device is None else device}") if on_gpu \
+        else torch.device("cpu")
+    if rank == src:
+        S = SparseMatrix.of(S)
+        if S.n_cols > 0x7FFFFFFF:
+            raise ValueError("column ids must fit in int32")
+        meta = torch.tensor([S.n_rows, S.n_cols, S.nnz], dtype=torch.int64, device=dev)
+        with warnings.catch_warnings():  # read-only (immutable) arrays: only ever copied out
+            warnings.simplefilter("ignore", UserWarning)
+            ro = torch.from_numpy(S.row_offsets).to(dev)
+            ci = torch.from_numpy(S.col_indices.astype(np.int32)).to(dev)
+            va = torch.from_numpy(S.values).to(dev)
+        if not on_gpu:  # gloo broadcasts in place on the source too: never alias the caller's arrays
+            ro, va = ro.clone(), va.clone()
+    else:
+        meta = torch.zeros(3, dtype=torch.int64, device=dev)
+    dist.broadcast(meta, src, group=group)
+    n_rows, n_cols, nnz = (int(x) for x in meta.tolist())
+    if rank != src:
+        ro = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+        ci = torch.empty(nnz, dtype=torch.int32, device=dev)
+        va = torch.empty(nnz, dtype=torch.float64, device=dev)
+    for t in (ro, ci, va):
+        dist.broadcast(t, src, group=group)
+    if on_gpu:
+        from .device_build import DeviceCSR
+
+        return DeviceCSR(n_rows, n_cols, ro, ci, va)
+    return SparseMatrix(n_rows, n_cols, ro.numpy(), ci.numpy().astype(np.int64), va.numpy(), check=False)
+
+
 def embed_column_sharded(S, coeffs, d: int, *, n_stages: int = 1, seed: int = 0, omega_kind: str = "reference",
                          dtype: str = "f64", normalize_rows: bool = True, group=None, device: int | None = None,
                          compute=None):
@@ -88,7 +136,11 @@ def embed_column_sharded(S, coeffs, d: int, *, n_stages: int = 1, seed: int = 0,
         E = assemble_columns(local, world, d, dtype, group)
         return E, combine_peaks(peaks, group)
     device = torch.cuda.current_device() if device is None else device
-    dm = DeviceMatrix(S, "float64" if dtype == "f64" else "float32", device)
+    dt = "float64" if dtype == "f64" else "float32"
+    if hasattr(S, "to_device_matrix"):  # a DeviceCSR (e.g. from broadcast_matrix): upload device to device
+        dm = S.to_device_matrix(dt, device)
+    else:
+        dm = DeviceMatrix(S, dt, device)
     plan = dm.plan(hi - lo)
     plan.run(coeffs, n_stages, omega_kind=_OMEGA[omega_kind], seed=seed, col0=lo, d_global=d)
     peaks, _, _ = plan.diagnostics()

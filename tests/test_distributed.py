@@ -279,3 +279,37 @@ def _bad_grid_worker(rank, world, port, result_path):
     finally:
         dist.destroy_process_group()
 
+
+
+# ---------------------------------------------------------------------------
+# C1: the matrix broadcast from one rank, then the column-sharded run
+# ---------------------------------------------------------------------------
+def _bcast_worker(rank, world, port, d, seed, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import broadcast_matrix, embed_column_sharded
+
+        S0, coeffs = _problem()
+        S = broadcast_matrix(_as_sparse(S0) if rank == 1 else None, src=1)
+        assert np.array_equal(S.row_offsets, S0.row_offsets)
+        assert np.array_equal(S.col_indices, S0.col_indices) and S.col_indices.dtype == np.int64
+        assert S.values.tobytes() == S0.values.tobytes()
+        Sc = O.CSR.of(S)
+        E, _ = embed_column_sharded(S, coeffs, d, seed=seed, normalize_rows=False,
+                                    compute=lambda lo, hi: _local_compute(Sc, coeffs, d, seed, lo, hi, "f64"))
+        np.save(result_path + f".{rank}.npy", E.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_matrix_then_column_shards(tmp_path):
+    d, seed, world = 21, 3, 3
+    out = str(tmp_path / "bc")
+    mp.start_processes(_bcast_worker, args=(world, _free_port(), d, seed, out), nprocs=world,
+                       start_method="spawn", join=True)
+    S, coeffs = _problem()
+    ref, _, _ = O.run_stage(S, coeffs, O.sample_projection(S.n_rows, d, seed))
+    for p in range(world):
+        assert np.array_equal(np.load(out + f".{p}.npy"), ref)

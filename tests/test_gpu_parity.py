@@ -614,6 +614,13 @@ class TestRowPartition:
             # the fused exchange through torch symmetric memory (no peers at world 1)
             E2, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="peer")
             assert np.array_equal(E2.cpu().numpy(), ref)
+            # C1: the CSR broadcast over NCCL into device memory, then the column-sharded run
+            from paper_1509_08360_b200.distributed import broadcast_matrix, embed_column_sharded
+
+            Sd = broadcast_matrix(S, src=0, device=0)
+            assert Sd.col_indices.dtype == torch.int32 and Sd.col_indices.is_cuda
+            E6, _ = embed_column_sharded(Sd, th, 24, seed=2, device=0, normalize_rows=False)
+            assert np.array_equal(E6.cpu().numpy(), ref)
             # the 2-D grid driver at 1 x 1 (row partition + column assembly + K4), both exchanges
             from paper_1509_08360_b200.distributed import embed_2d
 
