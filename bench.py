@@ -268,7 +268,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         traffic = ncu_traffic(dtype)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": B, "peak_source": peak_src}
+                "algorithmic_bytes_per_launch": B, "peak_source": peak_src,
+                "frac_of_8000": round(achieved / 8000.0, 4)}  # north_star's ~8 TB/s HBM3e figure
         if traffic:
             # north_star evidence: DRAM bytes actually moved per K1 launch (ncu) over
             # this run's live K1 time, against the ~8 TB/s HBM3e figure and the
