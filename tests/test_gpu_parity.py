@@ -818,7 +818,7 @@ def test_fuzz_random_csr_bit_exact():
     from hypothesis import given, settings
     from hypothesis import strategies as st
 
-    @settings(max_examples=40, deadline=None)
+    @settings(max_examples=int(os.environ.get("CSEMB_FUZZ_EXAMPLES", "40")), deadline=None)
     @given(n=st.integers(1, 400), density=st.floats(0.0, 0.2), heavy=st.booleans(), d=st.integers(1, 70),
            L=st.integers(0, 9), seed=st.integers(0, 2**31), f32=st.booleans())
     def check(n, density, heavy, d, L, seed, f32):
