@@ -503,7 +503,7 @@ def _run(S, coeffs, n_stages, block, *, dtype, device, normalize_rows, omega_kin
 
 
 def apply_expansion(S, expansion, block, *, stage: int = 0, n_workers: int = 1, counter=None,
-                    dtype="float64", device: int = 0, normalize_rows: bool = False) -> np.ndarray:
+                    dtype="float64", device: int | list[int] = 0, normalize_rows: bool = False) -> np.ndarray:
     """The drop-in seam: engine._apply_expansion (engine.py:231-258) on the GPU."""
     block = np.asarray(block, dtype=np.float64)
     if block.ndim != 2 or block.shape[0] != S.n_rows:
@@ -518,7 +518,7 @@ _apply_expansion = apply_expansion  # the reference's private name, for install(
 
 
 def fast_embed_eig(S, f, L: int, omega, *, quadrature=None, n_workers: int = 1, counter=None,
-                   dtype="float64", device: int = 0, normalize_rows: bool = False) -> EmbeddingMatrix:
+                   dtype="float64", device: int | list[int] = 0, normalize_rows: bool = False) -> EmbeddingMatrix:
     """f_L(S) @ omega for symmetric S with ||S|| <= 1 (engine.py:261-299)."""
     if S.n_rows != S.n_cols:
         raise ValueError("fast_embed_eig requires a square (symmetric) matrix")
@@ -537,7 +537,7 @@ def fast_embed_eig(S, f, L: int, omega, *, quadrature=None, n_workers: int = 1, 
 
 
 def fast_embed_cascaded(S, f, cfg: EmbedConfig, omega=None, *, quadrature=None, n_workers: int = 1,
-                        counter=None, dtype="float64", device: int = 0, normalize_rows: bool = False,
+                        counter=None, dtype="float64", device: int | list[int] = 0, normalize_rows: bool = False,
                         omega_kind: str = "reference") -> EmbeddingMatrix:
     """b cascade stages of order L/b on the b-th root of f (engine.py:302-349).
 
@@ -576,7 +576,7 @@ def fast_embed_cascaded(S, f, cfg: EmbedConfig, omega=None, *, quadrature=None, 
 
 
 def fast_embed_general(A, f, cfg: EmbedConfig, *, quadrature=None, n_workers: int = 1, counter=None,
-                       dtype="float64", device: int = 0, normalize_rows: bool = False,
+                       dtype="float64", device: int | list[int] = 0, normalize_rows: bool = False,
                        omega_kind: str = "reference"):
     """Row and column embeddings of a rectangular A via the dilation
     [0 A^T; A 0] and the odd extension of f (engine.py:352-391)."""
