@@ -172,6 +172,23 @@ class Context:
     def sync(self) -> None:
         check(self.lib.csemb_ctx_sync(self.handle), "csemb_ctx_sync")
 
+    def torch_stream(self):
+        """The context stream as a torch ExternalStream.  The library stream is
+        created non-blocking, so torch / NCCL work is NOT ordered with it
+        implicitly: run torch ops that touch library buffers under
+        `torch.cuda.stream(ctx.torch_stream())` (device-side ordering, no host
+        sync), or call `after_torch()` first."""
+        import torch
+
+        return torch.cuda.ExternalStream(self.stream, device=torch.device("cuda", self.device))
+
+    def after_torch(self) -> None:
+        """Order the context stream after everything queued so far on torch's
+        current stream of this device (device-side wait, the host does not block)."""
+        import torch
+
+        self.torch_stream().wait_stream(torch.cuda.current_stream(torch.device("cuda", self.device)))
+
     def close(self) -> None:
         if self.handle:
             self.lib.csemb_ctx_destroy(self.handle)

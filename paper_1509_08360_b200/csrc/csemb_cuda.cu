@@ -885,6 +885,16 @@ extern "C" int csemb_plan_destroy(csemb_plan *p) {
     return CSEMB_OK;
 }
 
+// A recorded graph has the plan's diagnostics / partials pointers built in:
+// whenever one of those buffers is reallocated, drop the graph and both
+// signatures, so the next run re-records against the new buffers.
+static void plan_drop_graph(csemb_plan *p) {
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    p->gexec = nullptr;
+    p->graph_sig.clear();
+    p->last_sig.clear();
+}
+
 template <typename T>
 static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stages,
                       const double *block_dev, int omega_kind, uint64_t seed, int64_t col0,
@@ -899,6 +909,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
     const int64_t n_chunks = (d_global + 31) / 32;
     const size_t need = (size_t)n_stages * (size_t)std::max(order, 0) * (size_t)n_chunks;
     if (need > p->peaks_cap) {
+        plan_drop_graph(p);
         dfree(c, p->peaks);
         p->peaks = nullptr;
         p->peaks_cap = 0;
@@ -923,6 +934,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
         if (rc) return rc;
         const size_t pbytes = (size_t)sc->n_chunks * (size_t)ld * sizeof(T);
         if (pbytes > p->partials_bytes) {
+            plan_drop_graph(p);
             dfree(c, p->partials);
             p->partials = nullptr;
             p->partials_bytes = 0;
@@ -1305,6 +1317,7 @@ static int plan_begin_t(csemb_plan *p, const double *block_dev, int omega_kind, 
     const int64_t n_chunks = (p->d_global + 31) / 32;
     const size_t need = (size_t)std::max(order, 0) * (size_t)n_chunks;
     if (need > p->peaks_cap) {
+        plan_drop_graph(p);
         dfree(c, p->peaks);
         p->peaks = nullptr;
         p->peaks_cap = 0;

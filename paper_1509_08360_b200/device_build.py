@@ -34,6 +34,10 @@ class DeviceCSR:
     def to_device_matrix(self, dtype="float64", device: int | None = None) -> DeviceMatrix:
         dev = self.values.device.index if device is None else device
         ci = self.col_indices
+        # the tensors may still be in flight on torch's stream (NCCL broadcasts of
+        # distributed.broadcast_matrix, builder kernels): the library stream must
+        # not read them before that work completes
+        torch.cuda.current_stream(self.values.device).synchronize()
         return DeviceMatrix.from_device(self.n_rows, self.n_cols, self.nnz, self.row_offsets.data_ptr(),
                                         ci.data_ptr(), ci.element_size(), self.values.data_ptr(), dtype, dev)
 
@@ -108,7 +112,35 @@ def from_host(S, device: int = 0) -> DeviceCSR:
                      torch.tensor(S.values, device=d))
 
 
-# -- seeded generators for configs 3 and 4 at full scale -----------
+# -- seeded generators for configs 2-5 at full scale ---------------
+def sbm_edges(n: int, blocks: int, deg_in: float, deg_out: float, seed: int, device: int = 0) -> torch.Tensor:
+    """Configs 2 / 5 on the GPU: the planted partition of graphs.sbm_edges
+    (contiguous equal blocks; each intra edge joins a uniform vertex to a
+    uniform vertex of its block, each inter edge to a uniform vertex of another
+    block), drawn with torch's CUDA generator."""
+    dev = torch.device(f"cuda:{device}")
+    g = torch.Generator(device=dev).manual_seed(seed)
+    bs = n // blocks
+    m_in, m_out = int(round(n * deg_in / 2.0)), int(round(n * deg_out / 2.0))
+    out = torch.empty((m_in + m_out, 2), dtype=torch.int64, device=dev)
+    u = torch.randint(0, n, (m_in,), generator=g, device=dev)
+    blk = torch.clamp(u // bs, max=blocks - 1)
+    lo = blk * bs
+    size = torch.where(blk == blocks - 1, n - lo, torch.full_like(lo, bs))
+    out[:m_in, 0] = u
+    out[:m_in, 1] = lo + (torch.rand(m_in, generator=g, device=dev, dtype=torch.float64) * size).to(torch.int64)
+    del u, blk, lo, size
+    u2 = torch.randint(0, n, (m_out,), generator=g, device=dev)
+    blk2 = torch.clamp(u2 // bs, max=blocks - 1)
+    lo2 = blk2 * bs
+    size2 = torch.where(blk2 == blocks - 1, n - lo2, torch.full_like(lo2, bs))
+    r = torch.randint(0, n, (m_out,), generator=g, device=dev) % (n - size2)
+    out[m_in:, 0] = u2
+    out[m_in:, 1] = torch.where(r >= lo2, r + size2, r)
+    return out
+
+
+
 def chung_lu_edges(n: int, seed: int, device: int = 0, exponent: float = 2.1, w_min: float = 2.0,
                    w_max: float = 1e4, mean: float = 20.0) -> torch.Tensor:
     """Config 3: Pareto(exponent) expected degrees in [w_min, w_max], rescaled

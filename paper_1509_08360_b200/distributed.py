@@ -145,14 +145,17 @@ def embed_column_sharded(S, coeffs, d: int, *, n_stages: int = 1, seed: int = 0,
     plan.run(coeffs, n_stages, omega_kind=_OMEGA[omega_kind], seed=seed, col0=lo, d_global=d)
     peaks, _, _ = plan.diagnostics()
     tdt = torch.float64 if dtype == "f64" else torch.float32
-    local = torch.empty((S.n_rows, hi - lo), dtype=tdt, device=f"cuda:{device}")
-    plan.copy_output_to(local.data_ptr(), hi - lo)
+    # every torch / NCCL op below runs on the library stream, so the gather, the
+    # concatenation and K4 are ordered after the recurrence on the device (the
+    # library stream is non-blocking: nothing orders it with torch's own stream)
+    with torch.cuda.stream(dm.ctx.torch_stream()):
+        local = torch.empty((S.n_rows, hi - lo), dtype=tdt, device=f"cuda:{device}")
+        plan.copy_output_to(local.data_ptr(), hi - lo)
+        E = assemble_columns(local, world, d, dtype, group)
+        if normalize_rows:
+            _lib.check(dm.lib.csemb_rownorm(dm.ctx.handle, E.data_ptr(), E.shape[0], d, d,
+                                            _lib.F64 if dtype == "f64" else _lib.F32), "csemb_rownorm")
     dm.ctx.sync()
-    E = assemble_columns(local, world, d, dtype, group)
-    if normalize_rows:
-        _lib.check(dm.lib.csemb_rownorm(dm.ctx.handle, E.data_ptr(), E.shape[0], d, d,
-                                        _lib.F64 if dtype == "f64" else _lib.F32), "csemb_rownorm")
-        dm.ctx.sync()
     dm.close()
     return E, combine_peaks(peaks, group)
 
@@ -183,25 +186,34 @@ class DeviceRowEngine:
     """One rank's share of a row-partitioned run on its GPU (C ABI step-wise
     plan over caller-owned torch buffers)."""
 
-    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q, peers=None, mc=None):
+    def __init__(self, S_local, row0, n_global, d, dtype, device, F, q, peers=None, mc=None, defer=False):
         from .engine import DeviceMatrix
 
         self.dm = DeviceMatrix(S_local, "float64" if dtype == "f64" else "float32", device)
         self.plan = self.dm.plan(d)
+        self.row0, self.n_global = row0, n_global
         if mc is not None:  # fused exchange through NVLS multicast addresses of F[0], F[1]
             self.plan.partition_multicast(row0, n_global, (F[0].data_ptr(), F[1].data_ptr()), mc)
-        elif peers is None:
-            self.plan.partition(row0, n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
-        else:  # fused exchange: F = this rank's two full buffers, peers = (parity-0, parity-1) pointer lists
+        elif peers is not None:  # fused exchange: F = this rank's two full buffers, peers = (parity-0, parity-1) pointer lists
             self.plan.partition_peers(row0, n_global, (F[0].data_ptr(), F[1].data_ptr()), peers[0], peers[1])
+        elif not defer:
+            self.bind(F, q)
         self.n_local, self.d = S_local.n_rows, d
+
+    def bind(self, F, q):
+        """All-gather exchange: steps gather from F and write the local Q(r) to q[r & 1]."""
+        self.plan.partition(self.row0, self.n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
 
     def begin(self, coeffs, omega_kind, seed, col0, d_global):
         self.plan.begin(coeffs, omega_kind=omega_kind, seed=seed, col0=col0, d_global=d_global)
 
     def step(self, r):
+        # enqueued on the library stream; the caller's exchange is ordered after
+        # it on the device (the driver runs its collectives on this stream)
         self.plan.step(r)
-        self.dm.ctx.sync()  # the caller's all-gather reads the local Q(r) next
+
+    def stream(self):
+        return self.dm.ctx.torch_stream()
 
     def end(self, normalize_rows):
         import torch
@@ -289,37 +301,60 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
             raise ValueError("the fused peer exchange runs on GPUs (torch symmetric memory)")
         mcast = exchange == "multicast"
         F2, ptrs = peer_buffers((world * n_pad, ld), tdt, dev, group, multicast=mcast)
+        torch.cuda.synchronize(dev)  # the buffers' zero-fill (torch's stream) before any library-stream write
         eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F2, None,
                               peers=None if mcast else ptrs, mc=ptrs if mcast else None)
         kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
-        eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
-        flag = torch.zeros(1, device=dev)
-        for r in range(1, len(coeffs)):
-            eng.step(r)  # host-synchronous: this rank's stores of Q(r) are complete
-            if r < len(coeffs) - 1:  # every rank done with step r before any starts step r+1
-                dist.all_reduce(flag, group=group)
-                torch.cuda.synchronize(dev)
-        E, peaks = eng.end(normalize_rows)
+        with torch.cuda.stream(eng.stream()):
+            eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
+            flag = torch.zeros(1, device=dev)
+            for r in range(1, len(coeffs)):
+                eng.step(r)
+                if r < len(coeffs) - 1:
+                    # device-side barrier: the all-reduce starts after this rank's step-r
+                    # kernels (which end with a system-scope fence) and completes only
+                    # when every rank has reached it; step r+1 waits for it on the
+                    # stream.  No host synchronisation per step.
+                    dist.all_reduce(flag, group=group)
+            E, peaks = eng.end(normalize_rows)
         return E, combine_peaks(peaks, group)
-    F = torch.zeros((world * n_pad, ld), dtype=tdt, device=dev)
-    q = [torch.zeros((n_pad, ld), dtype=tdt, device=dev) for _ in range(2)]
     if on_gpu:
-        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, F, q)
+        eng = DeviceRowEngine(S_local, row0, n_global, d, dtype, dev.index, None, None, defer=True)
+        stream = eng.stream()
     else:
-        eng = engine_factory(S_local, row0, n_global, d, dtype, F, q)
-    kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
-    eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
+        stream = None
     order = len(coeffs) - 1
-    parts = [F[p * n_pad:(p + 1) * n_pad] for p in range(world)]
-    for r in range(1, order + 1):
-        eng.step(r)
-        if r < order:  # refresh the replicated Q(r) for the next step
-            if dist.get_backend(group) == "nccl":
-                dist.all_gather_into_tensor(F, q[r & 1], group=group)
-            else:
-                dist.all_gather(parts, q[r & 1], group=group)
-    E, peaks = eng.end(normalize_rows)
+    kind = _lib.OMEGA_SPLITMIX if omega_kind == "reference" else _lib.OMEGA_PHILOX
+    # On GPUs the buffers, the steps and the per-step all-gather all run on the
+    # library stream: the all-gather of Q(r) starts when step r's kernels finish
+    # and step r+1 starts when it completes, ordered on the device with no host
+    # synchronisation in the loop.
+    with (torch.cuda.stream(stream) if stream is not None else _nullcontext()):
+        F = torch.zeros((world * n_pad, ld), dtype=tdt, device=dev)
+        q = [torch.zeros((n_pad, ld), dtype=tdt, device=dev) for _ in range(2)]
+        if on_gpu:
+            eng.bind(F, q)
+        else:
+            eng = engine_factory(S_local, row0, n_global, d, dtype, F, q)
+        eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
+        parts = [F[p * n_pad:(p + 1) * n_pad] for p in range(world)]
+        for r in range(1, order + 1):
+            eng.step(r)
+            if r < order:  # refresh the replicated Q(r) for the next step
+                if dist.get_backend(group) == "nccl":
+                    dist.all_gather_into_tensor(F, q[r & 1], group=group)
+                else:
+                    dist.all_gather(parts, q[r & 1], group=group)
+        E, peaks = eng.end(normalize_rows)
     return E, combine_peaks(peaks, group)
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
 
 
 # ---------------------------------------------------------------------------

@@ -12,7 +12,16 @@ between the host arrays and the result runs on the GPU through the C ABI
   sample_projection (engine.py:79-99)       -> csemb_sample_projection (K2)
   estimate_spectral_norm (engine.py:165-192) -> csemb_spectral_norm (K3)
 
-Additive keywords (defaults reproduce the reference bit-for-bit):
+Exactness: fp64 results are bit-identical to the reference for every matrix
+whose rows all have at most `split_threshold` stored entries (default 2048:
+configs 1-2 and every reference test).  Longer rows are summed as 1024-entry
+chunk partials added in chunk order (load balance for power-law rows), which
+changes only those rows' rounding -- measured within 1e-13 relative Frobenius
+on configs 3/4 shapes against the oracle, inside north_star's 1e-10 gate.
+`Plan.set_load_balance(split_threshold=0)` (CSEMB_OPT_SPLIT_THRESHOLD 0)
+restores strict stored-order sums for every row.
+
+Additive keywords (defaults reproduce the reference's results, see above):
   dtype="float64"|"float32", normalize_rows=False, device=0,
   omega_kind="reference"|"philox" (only where the engine samples Omega itself),
   start="reference"|"philox" (norm-estimate starting block).
@@ -24,6 +33,7 @@ from __future__ import annotations
 
 import ctypes as C
 import logging
+import threading
 import math
 import weakref
 from dataclasses import dataclass, field
@@ -241,6 +251,7 @@ class Plan:
         self.handle = h
         self.last = None
         self.exact_peaks = False
+        self.lock = threading.Lock()  # run -> copy -> diagnostics sequences from several threads
 
     def set_option(self, option: int, value: int) -> None:
         _lib.check(self.lib.csemb_plan_set_option(self.handle, int(option), int(value)), "csemb_plan_set_option")
@@ -429,54 +440,79 @@ def _log_steps(peaks: np.ndarray, d: int, col_base: int = 0) -> None:
                              float(peaks[st, r - 1, ch]))
 
 
+def _first_bad(keys: np.ndarray) -> tuple[int, int]:
+    """(first bad r, its stage) in the reference's order: stages in turn, within
+    a stage the 32-column chunks in column order, each run to completion before
+    the next (engine.py:250-252, 333-336); (0, 0) if every step is finite."""
+    bad = keys >= np.uint64(0x7FF0000000000000)  # NaN / inf |Q| keys
+    n_stages, order, n_chunks = keys.shape
+    for st in range(n_stages):
+        for ch in range(n_chunks):
+            rs = np.flatnonzero(bad[st, :, ch])
+            if rs.size:
+                return int(rs[0]) + 1, st + 1
+    return 0, 0
+
+
 def _run_devices(S, coeffs, n_stages, block, devices, *, dtype, normalize_rows, omega_kind, seed, d):
     """One process, several GPUs: the d columns are independent (Theorem 1,
     PAPER.md:100), so each device runs its column shard concurrently (the
     ctypes calls release the GIL) with the projection hashed on global
-    columns; the shards are assembled on the host and, if asked, row-
-    normalised by K4 on the first device.  Bit-identical to one device."""
+    columns.  Device-resident assembly: every shard's E slice is copied
+    device-to-device (NVLink P2P where available) into one n x d buffer on the
+    first device, K4 row-normalises it there, and a single D2H copy returns the
+    result.  Divergence is reported at the first bad step of the max-combined
+    per-chunk diagnostics, in the reference's order.  Bit-identical to one
+    device."""
     from concurrent.futures import ThreadPoolExecutor
+
+    import torch
 
     from .distributed import column_shards
 
-    width = 4 if dtype_code(dtype) == _lib.F32 else 2
+    f32 = dtype_code(dtype) == _lib.F32
+    width = 4 if f32 else 2
+    tdt = torch.float32 if f32 else torch.float64
     shards = [(dev, lo, hi) for dev, (lo, hi) in zip(devices, column_shards(d, len(devices), width)) if hi > lo]
     debug = logger.isEnabledFor(logging.DEBUG)
+    home = torch.device("cuda", devices[0])
 
     def one(item):
         dev, lo, hi = item
-        plan = device_matrix(S, dtype, dev).plan(hi - lo)
-        plan.set_exact_peaks(debug)
-        blk = None if block is None else np.ascontiguousarray(block[:, lo:hi])
-        try:
-            out = plan.apply(coeffs, n_stages, blk, omega_kind=omega_kind, seed=seed, col0=lo, d_global=d)
-            return out, plan.peaks, None
-        except DivergenceError as e:
-            return None, None, e
+        dm = device_matrix(S, dtype, dev)
+        plan = dm.plan(hi - lo)
+        with plan.lock, torch.cuda.device(dev), torch.cuda.stream(dm.ctx.torch_stream()):
+            plan.set_exact_peaks(debug)
+            blk = None
+            if block is not None:
+                blk = torch.from_numpy(np.ascontiguousarray(block[:, lo:hi])).to(f"cuda:{dev}")
+            plan.run(coeffs, n_stages, block_dev=None if blk is None else blk.data_ptr(), omega_kind=omega_kind,
+                     seed=seed, col0=lo, d_global=d)
+            part = torch.empty((S.n_rows, hi - lo), dtype=tdt, device=f"cuda:{dev}")
+            plan.copy_output_to(part.data_ptr(), hi - lo)
+            dm.ctx.sync()
+            peaks, _, _ = plan.diagnostics()
+        return part, peaks
 
     with ThreadPoolExecutor(len(shards)) as pool:
         results = list(pool.map(one, shards))
-    bad = [e for _, _, e in results if e is not None]
-    if bad:  # the first non-finite step over all columns, as the reference reports it
-        import re
-
-        raise min(bad, key=lambda e: int(re.search(r"r=(\d+)", str(e)).group(1)))
-    out = np.empty((S.n_rows, d), dtype=np.float64)
-    for (dev, lo, hi), (part, _, _) in zip(shards, results):
-        out[:, lo:hi] = part
-    if debug:  # per-chunk maxima: each shard reports its global chunks, max-combined (NaN keys dominate)
-        keys = np.maximum.reduce([np.ascontiguousarray(pk).view(np.uint64) for _, pk, _ in results])
+    keys = np.maximum.reduce([np.ascontiguousarray(pk).view(np.uint64) for _, pk in results])
+    bad_r, _ = _first_bad(keys)
+    if bad_r:
+        raise DivergenceError(_lib.DIVERGENCE_MESSAGE.format(r=bad_r))
+    if debug:  # per-chunk maxima: each shard reports its global chunks, max-combined
         _log_steps(keys.view(np.float64), d)
-    if normalize_rows:
+    E = torch.empty((S.n_rows, d), dtype=tdt, device=home)
+    for (dev, lo, hi), (part, _) in zip(shards, results):
+        E[:, lo:hi].copy_(part)  # peer copy (NVLink P2P where available)
+    for dev, _, _ in shards:  # the copies ran on torch's streams: finish them before K4 reads E
+        torch.cuda.synchronize(dev)
+    if normalize_rows and S.n_rows > 0:
         ctx = _lib.context(devices[0])
-        import torch
-
-        E = torch.from_numpy(out).to(f"cuda:{devices[0]}")
-        torch.cuda.synchronize(E.device)
-        _lib.check(ctx.lib.csemb_rownorm(ctx.handle, E.data_ptr(), S.n_rows, d, d, _lib.F64), "csemb_rownorm")
+        _lib.check(ctx.lib.csemb_rownorm(ctx.handle, E.data_ptr(), S.n_rows, d, d, _lib.F32 if f32 else _lib.F64),
+                   "csemb_rownorm")
         ctx.sync()
-        out = E.cpu().numpy()
-    return out
+    return E.to(torch.float64).cpu().numpy()
 
 
 def _run(S, coeffs, n_stages, block, *, dtype, device, normalize_rows, omega_kind=_lib.OMEGA_GIVEN,

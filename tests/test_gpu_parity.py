@@ -502,6 +502,7 @@ class TestRowPartition:
             plan = dm.plan(d)
             q = [torch.zeros((n_pad, d), dtype=tdt, device="cuda") for _ in range(2)]
             plan.partition(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+            torch.cuda.synchronize()  # torch's zero-fills before the library stream writes
             plan.begin(th, omega_kind=1, seed=3)
             ranks.append((lo, hi, dm, plan, q))
         for r in range(1, L + 1):
@@ -621,6 +622,9 @@ class TestRowPartition:
             assert Sd.col_indices.dtype == torch.int32 and Sd.col_indices.is_cuda
             E6, _ = embed_column_sharded(Sd, th, 24, seed=2, device=0, normalize_rows=False)
             assert np.array_equal(E6.cpu().numpy(), ref)
+            # K4 after the gather, ordered on the library stream (no host sync in between)
+            E7, _ = embed_column_sharded(Sd, th, 24, seed=2, device=0, normalize_rows=True)
+            np.testing.assert_allclose(E7.cpu().numpy(), O.row_normalize(ref), rtol=0, atol=1e-15)
             # the 2-D grid driver at 1 x 1 (row partition + column assembly + K4), both exchanges
             from paper_1509_08360_b200.distributed import embed_2d
 
@@ -873,6 +877,31 @@ def test_graph_replay_bit_exact(config1):
     dm.close()
 
 
+def test_graph_survives_buffer_reallocation(config1):
+    """A recorded graph has the diagnostics buffer built in: runs of order
+    a, a, b > a, a (the b run reallocates the buffer) must neither replay into
+    the freed buffer nor report stale diagnostics."""
+    z, meta = config1
+    S = sparse_from(z)
+    dm = pb.DeviceMatrix(S, "float64")
+    plan = dm.plan(40)
+    plan.set_option(pb._lib.OPT_GRAPH, 1)
+    plan.set_exact_peaks(True)
+    om = O.sample_projection(2000, 40, 0)
+    refs = {}
+    for L in (4, 4, 4, 9, 4, 4, 9, 9, 4, 15, 4):
+        th = z["coeffs"][:L + 1]
+        if L not in refs:
+            refs[L] = O.run_stage(O.CSR.of(S), th, om)
+        ref, ref_peaks, _ = refs[L]
+        plan.run(th, 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+        assert np.array_equal(plan.download(), ref), L
+        peaks, bad, _ = plan.diagnostics()
+        assert bad == 0 and peaks.shape == (1, L, 2)
+        assert np.array_equal(peaks[0], ref_peaks), L
+    dm.close()
+
+
 def test_out_of_memory_is_reported_and_context_survives(config1):
     """An impossible allocation surfaces as MemoryError (CSEMB_ERR_NOMEM after
     the pool is trimmed and the allocation retried); the context stays usable."""
@@ -996,46 +1025,4 @@ def test_config2_full_scale_fp64_bit_exact_and_fp32_gates():
     assert r <= FP32_REL and c <= COS_TOL, (r, c)
 
 
-@pytest.mark.parametrize("config", [3, 4])
-def test_configs34_full_scale_fp32_gates(config):
-    # configs 3 / 4 at full size (device-built inputs, as tools/bench_configs.py):
-    # fp32 vs fp64 on identical inputs through the north_star gates; the fp64
-    # path's stored-order arithmetic is pinned bit-exact by the tests above
-    import math
-
-    import torch
-
-    from paper_1509_08360_b200 import device_build as db
-
-    if config == 3:
-        S = db.normalized_adjacency(db.chung_lu_edges(10_000_000, seed=3), 10_000_000)
-        f, d, L = pb.commute_time(0.01), 80, 180
-    else:
-        S = db.dilate(db.bag_of_words(2_000_000, 500_000, seed=4))
-
-        class CutAbove:  # f(x) = x * 1{x >= 0.3} (not a built-in kind)
-            def __call__(self, x):
-                x = np.asarray(x, dtype=np.float64)
-                return np.where(x >= 0.3, x, 0.0)
-
-            def breakpoints(self):
-                return (0.3,)
-
-        f, d, L = pb.odd_extension(CutAbove()), 96, 120
-    torch.cuda.synchronize()
-    th = pb.legendre_coefficients(f, L).coeffs
-    out = {}
-    for dt in ("float64", "float32"):
-        dm = S.to_device_matrix(dt)
-        if config == 4:  # spectrum scaled by the 30-iteration estimate, identical for both dtypes
-            if dt == "float64":
-                est = dm.spectral_norm(30, max(1, math.ceil(6.0 * math.log(S.n_rows))), 11, 1.01)
-            dm.scale(1.0 / est)
-        plan = dm.plan(d)
-        plan.run(th, 1, omega_kind=2, seed=7)
-        out[dt] = _device_result(plan, d)
-        dm.close()
-    assert torch.isfinite(out["float64"]).all()
-    r, c = _fp32_gates(out["float32"], out["float64"], S.n_rows, 5)
-    print(f"config {config} full scale: fp32 rel {r:.3e}, cosine error {c:.3e}")
-    assert r <= FP32_REL and c <= COS_TOL, (r, c)
+# configs 3 / 4 / 5 at full shape against the oracle: tests/test_gpu_scale.py

@@ -1,0 +1,198 @@
+"""BASELINE configs 3, 4 and 5 at full shape against the oracle (B200 only).
+
+The default device path -- row splitting of heavy rows into chunk partials,
+bucketed schedules, the device power-iteration norm estimate (config 4) and
+the row partition (config 5) -- is compared with the C oracle, the reference's
+`_run_stage` restatement (oracle/csemb_oracle.c, engine.py:205-228), on the
+same matrix, projection and coefficients.  The order is truncated to
+L_TRUNC so the oracle finishes in tens of seconds on the box's cores; every
+step is the same SpMM + elementwise work (engine.py:213-227), so a truncated
+order exercises the whole path.
+
+Gates (north_star): relative Frobenius error <= 1e-10 in fp64 and <= 1e-4 in
+fp32, pairwise cosine error <= 1e-4 on 10^4 sampled row pairs.  fp64 with a
+split heavy row is not bit-identical (chunk partials change that row's
+rounding), hence the tolerance rather than array_equal; rows that are not
+split keep the reference's stored-order arithmetic (pinned bit-exact in
+test_gpu_parity.py).
+"""
+
+import math
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1509_08360_b200 as pb
+
+pytestmark = pytest.mark.gpu
+
+FP64_REL = 1e-10     # north_star: relative Frobenius error in fp64
+FP32_REL = 1e-4      # north_star: relative Frobenius error in fp32
+COS_TOL = 1e-4       # north_star: pairwise cosine error on 10^4 sampled pairs
+L_TRUNC = 10         # truncated order (oracle runtime); the device runs the same order
+
+
+@pytest.fixture(autouse=True)
+def _lib_ready(gpu_lib):
+    O.set_threads(os.cpu_count() or 1)
+    yield
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def cos_err(a, b, n, seed):
+    pairs = O.sample_pairs(n, 10_000, seed)
+    return float(np.max(np.abs(O.pair_cosines(a, pairs) - O.pair_cosines(b, pairs))))
+
+
+class CutAbove:
+    """Config 4's f(x) = x * 1{x >= 0.3} (not a built-in kind)."""
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return np.where(x >= 0.3, x, 0.0)
+
+    def breakpoints(self):
+        return (0.3,)
+
+
+def _device_vs_oracle(S, th, d, seed, *, norm_iters=0, label=""):
+    """Run the default device path in fp64 and fp32 on the device-built CSR S
+    and the oracle on the same (scaled) values; return the three errors."""
+    import torch
+
+    torch.cuda.synchronize()
+    lens = (S.row_offsets[1:] - S.row_offsets[:-1])
+    longest = int(lens.max())
+    out, scale, values = {}, None, None
+    for dt in ("float64", "float32"):
+        dm = S.to_device_matrix(dt)
+        if norm_iters:
+            if scale is None:  # the device estimate (fp64), the same scalar for both dtypes
+                k = max(1, math.ceil(6.0 * math.log(max(S.n_rows, 2))))
+                scale = 1.0 / dm.spectral_norm(norm_iters, k, 11, 1.01)
+            dm.scale(scale)
+        if dt == "float64":
+            values = dm.download_values()  # exactly S.values * scale (csemb_matrix_scale)
+        plan = dm.plan(d)  # default load balance: split + bucketed schedule
+        t0 = time.perf_counter()
+        plan.run(th, 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=seed)
+        out[dt] = plan.download()
+        _, bad, _ = plan.diagnostics()
+        assert bad == 0
+        print(f"{label} {dt}: device {time.perf_counter() - t0:.2f} s")
+        dm.close()
+    host = S.to_host()
+    host = O.CSR(host.n_rows, host.n_cols, host.row_offsets, host.col_indices, values)
+    t0 = time.perf_counter()
+    ref, _, bad = O.run_stage(host, th, O.sample_projection(S.n_rows, d, seed))
+    print(f"{label} oracle: {time.perf_counter() - t0:.1f} s on {O.num_threads()} threads; longest row {longest}")
+    assert bad == 0
+    r64, r32 = rel(out["float64"], ref), rel(out["float32"], ref)
+    c32 = cos_err(out["float32"], ref, S.n_rows, 5)
+    print(f"{label}: fp64 rel {r64:.3e}, fp32 rel {r32:.3e}, fp32 cosine error {c32:.3e}")
+    return r64, r32, c32, longest
+
+
+def test_config3_full_shape_vs_oracle():
+    # Chung-Lu n = 1e7, Pareto(2.1) degrees in [2, 1e4] rescaled to mean 20,
+    # commute-time f clipped at x <= 0.99, d = 80; heavy rows are split
+    from paper_1509_08360_b200 import device_build as db
+
+    n = 10_000_000
+    S = db.normalized_adjacency(db.chung_lu_edges(n, seed=3), n)
+    th = pb.legendre_coefficients(pb.commute_time(0.01), L_TRUNC).coeffs
+    r64, r32, c32, longest = _device_vs_oracle(S, th, 80, 9, label="config 3")
+    assert longest > 2048  # the split (chunk-partial) path ran
+    assert r64 <= FP64_REL, r64
+    assert r32 <= FP32_REL and c32 <= COS_TOL, (r32, c32)
+
+
+def test_config4_full_shape_vs_oracle():
+    # bag of words 2e6 x 5e5 (Poisson(150) lengths, Zipf(1.1) terms, tf-idf,
+    # L2 rows) -> dilation [0 A^T; A 0] (n = 2.5e6, ~4e8 stored entries),
+    # spectrum scaled by the 30-iteration device norm estimate (k = 89),
+    # odd-extended f(x) = x 1{x >= 0.3}, d = 96 (fast_embed_general's path,
+    # engine.py:352-391); the term rows hold up to ~2e6 entries
+    from paper_1509_08360_b200 import device_build as db
+
+    S = db.dilate(db.bag_of_words(2_000_000, 500_000, seed=4))
+    th = pb.legendre_coefficients(pb.odd_extension(CutAbove()), L_TRUNC).coeffs
+    r64, r32, c32, longest = _device_vs_oracle(S, th, 96, 13, norm_iters=30, label="config 4")
+    assert longest > 100_000
+    assert r64 <= FP64_REL, r64
+    assert r32 <= FP32_REL and c32 <= COS_TOL, (r32, c32)
+
+
+def _config5_rows() -> int:
+    """Config-5 slice size: 2e7 rows where the box has the host memory for the
+    oracle's fp64 blocks (~6 n x 64 doubles), else 1e7."""
+    import psutil
+
+    return 20_000_000 if psutil.virtual_memory().available > 96 << 30 else 10_000_000
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_config5_slice_row_partition_vs_oracle(dtype):
+    # config 5's structure (SBM, blocks of 1e5 vertices, average degree 16,
+    # d = 64, f = 1{x >= 0.95}) on a 1-2e7-vertex slice, row-partitioned over
+    # 3 ranks emulated on one GPU: each rank's plan gathers from a replicated
+    # full Q(r-1) and the per-step all-gather is emulated by device copies (no
+    # rank ever waits on another).  fp64 bit-identical to the oracle; fp32
+    # through the north_star gates.
+    import torch
+
+    from paper_1509_08360_b200 import device_build as db
+    from paper_1509_08360_b200.distributed import row_blocks
+
+    n = _config5_rows()
+    d, L, world, seed = 64, 6, 3, 21
+    S = db.normalized_adjacency(db.sbm_edges(n, n // 100_000, 12.0, 4.0, seed=5), n)
+    th = pb.legendre_coefficients(pb.indicator_above(0.95), L).coeffs
+    tdt = torch.float64 if dtype == "float64" else torch.float32
+    n_pad, blocks = row_blocks(n, world)
+    F = torch.zeros((world * n_pad, d), dtype=tdt, device="cuda")
+    ranks = []
+    ro, ci, va = S.row_offsets, S.col_indices, S.values
+    for lo, hi in blocks:
+        a, b = int(ro[lo]), int(ro[hi])
+        part = db.DeviceCSR(hi - lo, n, (ro[lo:hi + 1] - a).contiguous(), ci[a:b].contiguous(), va[a:b].contiguous())
+        dm = part.to_device_matrix(dtype)
+        plan = dm.plan(d)
+        q = [torch.zeros((n_pad, d), dtype=tdt, device="cuda") for _ in range(2)]
+        plan.partition(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        torch.cuda.synchronize()  # torch's zero-fills before the library stream writes
+        plan.begin(th, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=seed)
+        ranks.append((lo, hi, dm, plan, q))
+    for r in range(1, L + 1):
+        for _, _, _, plan, _ in ranks:
+            plan.step(r)
+        for _, _, dm, _, _ in ranks:
+            dm.ctx.sync()
+        if r < L:
+            for lo, hi, _, _, q in ranks:  # the all-gather, emulated by device copies
+                F[lo:hi] = q[r & 1][:hi - lo]
+            torch.cuda.synchronize()
+    got = []
+    for _, _, dm, plan, _ in ranks:
+        plan.end(False)
+        got.append(plan.download())
+        dm.close()
+    del F
+    got = np.concatenate(got)
+    host = S.to_host()
+    del S
+    ref, _, bad = O.run_stage(O.CSR.of(host), th, O.sample_projection(n, d, seed))
+    assert bad == 0
+    if dtype == "float64":
+        assert np.array_equal(got, ref)
+    else:
+        r32 = rel(got, ref)
+        c32 = cos_err(got, ref, n, 7)
+        print(f"config 5 slice n={n} fp32: rel {r32:.3e}, cosine error {c32:.3e}")
+        assert r32 <= FP32_REL and c32 <= COS_TOL, (r32, c32)
