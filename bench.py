@@ -4,22 +4,30 @@
 
 Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
 SBM n=1e6 in 100 blocks, expected degree 15 intra + 5 inter, normalized
-adjacency (T ~ 2e7 stored nnz), d=80, L=180, f(x)=1{x>=0.95}, Philox
-projection generated on the device, row-normalised output.  One "step" = one
-whole embedding: projection init + 180 fused K1 steps + row normalisation.
-Headline dtype is f64 (the reference's arithmetic, bit-exact); an "fp32"
-object reports the same workload in fp32.
+adjacency (T ~ 2e7 stored nnz), d=80, L=180, f(x)=1{x>=0.95}, the reference's
+SplitMix64 projection (sample_projection(n, d, 7), generated on the device
+bit-identically), row-normalised output.  One "step" = one whole embedding:
+projection init + 180 fused K1 steps + row normalisation.  Headline dtype is
+f64 (the reference's arithmetic, bit-exact); an "fp32" object reports the same
+workload in fp32.  Both arms run this identical workload (same_config).
 
 value  = T*d*L / device time per step (CUDA events, inputs resident in HBM;
          the working set -- 2 x 640 MB Q buffers + 640 MB E + 240 MB CSR in
          f64 -- is far larger than the 126 MB L2, so no flush is needed).
-e2e    = same metric through the reference-facing C ABI call with HOST
-         buffers, the reference's default entry (fast_embed_cascaded with
-         omega=None): CSR upload (H2D) every step, Omega generated on the
-         device bit-identical to the reference's sample_projection, E D2H.
+e2e    = same metric through the public API a reference user calls,
+         fast_embed_cascaded(S, f, cfg, normalize_rows=True) with omega=None,
+         on a fresh SparseMatrix every step (numpy arrays over pinned host
+         memory): CSR H2D, coefficients, Omega on the device, E D2H into a new
+         numpy array -- all inside the timed region.  At N>1 (torchrun) the same
+         through distributed.embed_column_sharded from the host CSR on every
+         rank, E assembled by NCCL and read back on rank 0; max over ranks.
 roofline: K1's algorithmic bytes per launch, B = T*(4+8) + 5*n*d*8 (f64) /
          T*(4+4) + 5*n*d*4 (f32), over K1's average launch time (CUDA events
          on the library stream), against MEASURED_PEAKS.json hbm_gbs.
+configs34: BASELINE configs 3 and 4 at full size (fp32, device-built inputs):
+         embed wall time (incl. config 4's 30-iteration norm), K1 per step and
+         its roofline.  builders: SURVEY 8(f) rank 1, the device edge-list ->
+         normalized adjacency against the reference's host builder.
 N>1 (torchrun): columns are sharded across ranks (the matrix is replicated),
 one NCCL all-gather assembles E; value = total units / max-over-ranks time.
 """
@@ -42,6 +50,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fused SpMM-recurrence nnz*d*L/s (config 2)"
 UNIT = "nnz*d*L/s"
+WORKLOAD = ("config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, f=1{x>=0.95}, "
+            "Omega = sample_projection(n, d, 7), row-normalised")
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def log(*a):
@@ -175,6 +186,45 @@ def gather_roof(nnz: int, ld: int, dtype: str, k1_ms: float):
     return roof
 
 
+def live_ceilings(ctx, row_bytes: int):
+    """L2 -> SM and HBM ceilings measured now, on this device, next to the
+    timed region (same clocks and power state): csemb_diag_bandwidth probes
+    (csrc/diag.cu).  Returns GB/s for the streaming / K1-shaped gather / copy
+    probes."""
+    import ctypes as C
+
+    from paper_1509_08360_b200 import _lib
+
+    out = {}
+    for name, kind, nbytes, reps in (("l2_stream", 0, 48 << 20, 20), ("l2_gather", 1, 48 << 20, 500),
+                                     ("hbm_copy", 2, 1 << 30, 1)):
+        v = C.c_double(0.0)
+        _lib.check(ctx.lib.csemb_diag_bandwidth(ctx.handle, kind, nbytes, row_bytes, reps, C.byref(v)),
+                   "csemb_diag_bandwidth")
+        out[name] = round(v.value, 1)
+    return out
+
+
+def fabric_roof(ctx, nnz: int, n: int, d: int, ld: int, dtype: str, k1_ms: float, L: int):
+    """K1's L2 -> SM side (the resource a gather SpMM saturates first): bytes
+    that cross the fabric per launch -- every stored entry gathers one
+    ld-wide row of Q(r-1), plus the matrix stream, Q(r-2), and the folded E /
+    own-row reads (1/3 of the steps) -- over K1's live time, against the
+    streaming and K1-shaped gather ceilings measured live next to it."""
+    es = 8 if dtype == "f64" else 4
+    gathered = nnz * ld * es
+    streams = nnz * (4 + es) + n * ld * es * (1 + 2.0 / 3.0)
+    total = gathered + streams
+    ach = total / (k1_ms * 1e-3) / 1e9
+    live = live_ceilings(ctx, min(768, ld * es))
+    return {"bytes_per_launch": int(total), "gathered_bytes_per_launch": gathered, "achieved": round(ach, 1),
+            "unit": "GB/s", "live_ceilings_gbs": live,
+            "frac_of_live_gather": round(ach / live["l2_gather"], 4),
+            "frac_of_live_stream": round(ach / live["l2_stream"], 4),
+            "hbm_frac_of_live_copy": None,  # filled by the caller (algorithmic HBM bytes)
+            "source": "csemb_diag_bandwidth (csrc/diag.cu), measured right after the timed region"}
+
+
 def k1_bytes(nnz: int, n: int, d: int, ld: int, dtype: str) -> int:
     """north_star model: T*(idx+val) + 5*n*d*dtype (Y_l, Y_{l-1}, E read; Y_{l+1}, E written)."""
     es = 8 if dtype == "f64" else 4
@@ -218,7 +268,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         gather_buf = None
 
         def one_step():
-            plan.run(coeffs, 1, omega_kind=_lib.OMEGA_PHILOX, seed=7, col0=lo, d_global=d,
+            plan.run(coeffs, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7, col0=lo, d_global=d,
                      normalize_rows=(world == 1))
             if world > 1:
                 nonlocal gather_buf
@@ -280,6 +330,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                             "traffic_over_model": round(traffic / B, 3)}
         W = 2 if dtype == "f64" else 4
         roof["gather"] = gather_roof(nnz, (hi - lo + W - 1) // W * W, dtype, k1_ms)
+        roof["l2_fabric"] = fabric_roof(dm.ctx, nnz, n, hi - lo, (hi - lo + W - 1) // W * W, dtype, k1_ms, L)
+        roof["l2_fabric"]["hbm_frac_of_live_copy"] = round(achieved / roof["l2_fabric"]["live_ceilings_gbs"]["hbm_copy"], 4)
         out = {
             "value": units / (ms * 1e-3), "ms_per_step": ms, "k1_ms": k1_ms,
             "gpu_launches_per_step": launches_per_step,
@@ -306,23 +358,30 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             f"{res32['roofline']['achieved']:.0f} GB/s ({res32['roofline']['frac']:.3f})")
 
     e2e = None
-    if not args.skip_e2e and world == 1:
-        e2e = run_e2e(args, S, coeffs, units, local_rank)
-        log(f"[bench] e2e: {e2e['ms_per_step']:.1f} ms/step -> {e2e['value']:.3e} {UNIT}")
+    if not args.skip_e2e:
+        e2e = run_e2e(args, S, f, units, local_rank) if world == 1 else \
+            run_e2e_sharded(args, S, coeffs, units, rank, world, local_rank)
+        if rank == 0:
+            log(f"[bench] e2e: {e2e['ms_per_step']:.1f} ms/step -> {e2e['value']:.3e} {UNIT}")
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline(S, d, coeffs, args.cpu_seconds)
         log(f"[bench] cpu baseline: {cpu['value']:.3e} {UNIT} on {cpu['cores']} threads ({cpu['sample']})")
 
+    extra34, builders = None, None
+    if rank == 0 and world == 1 and not args.skip_configs34:
+        extra34 = run_configs34(args, peak, peak_src)
+    if rank == 0 and world == 1 and not args.skip_builders:
+        builders = run_builders(args)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": res64["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res64["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded O(T) SBM sampler; Philox projection on device)",
-            "config": {"workload": "config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, "
-                                   "f=1{x>=0.95}, row-normalised",
+            "data": "synthetic (seeded O(T) SBM sampler; the reference's SplitMix64 projection, on device)",
+            "config": {"workload": WORKLOAD,
                        "n": n, "nnz": nnz, "d": d, "L": L,
                        "parallelism": f"column-shard x{world}" if world > 1 else "1 GPU",
                        "l2": "working set >> 126 MB L2 (no flush needed)"},
@@ -335,6 +394,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         }
         if down is not None:
             line["downstream"] = down
+        if extra34 is not None:
+            line["configs34"] = extra34
+        if builders is not None:
+            line["builders"] = builders
         if res32 is not None:
             line["fp32"] = {"value": res32["value"], "ms_per_step": res32["ms_per_step"], "k1_ms": res32["k1_ms"],
                             "roofline": res32["roofline"], "clocks": res32["clocks"]}
@@ -423,52 +486,215 @@ def run_downstream(dm, plan, n, K=100, iters=8):
                                 "flops_per_assign": 2.0 * n * K * d}}
 
 
-def run_e2e(args, S, coeffs, units, device):
-    """Reference-facing call with host buffers, the reference's default entry
-    fast_embed_cascaded(S, f, cfg) (omega=None: Omega = sample_projection(n, d,
-    seed), engine.py:319-320): upload the CSR, generate Omega on the device with
-    the reference's SplitMix64 hash (bit-identical), run, download E."""
+def run_e2e(args, S, f, units, device):
+    """The reference user's call, end to end: fast_embed_cascaded(S, f, cfg,
+    normalize_rows=True) with omega=None (Omega = sample_projection(n, d,
+    seed), engine.py:319-320, generated on the device bit-identically).  The
+    user's SparseMatrix is built once (its arrays live in pinned host memory,
+    sparse._frozen); every step uploads the CSR (H2D), computes the
+    coefficients, embeds, returns E in a new numpy array (D2H) and drops the
+    cached device copy (release_device_copy), so the next step uploads again."""
     import torch
 
     import paper_1509_08360_b200 as pb
-    from paper_1509_08360_b200 import _lib
 
     n, d = S.n_rows, args.d
-    pin = lambda a: torch.from_numpy(np.array(a)).pin_memory()  # noqa: E731
-    ro, ci, va = pin(S.row_offsets), pin(S.col_indices), pin(S.values)
-    out = torch.empty((n, d), dtype=torch.float64).pin_memory()
-    ctx = _lib.context(device)
-    lib = ctx.lib
-    import ctypes as C
-
-    h2d = ro.numel() * 8 + ci.numel() * 8 + va.numel() * 8
-    d2h = out.numel() * 8
-    c = np.ascontiguousarray(coeffs)
+    Su = pb.SparseMatrix(n, n, S.row_offsets, S.col_indices, S.values, check=False)
+    cfg = pb.EmbedConfig(L=args.L, d=d, seed=7)
 
     def step():
-        h = C.c_void_p()
-        _lib.check(lib.csemb_matrix_upload(ctx.handle, n, n, S.nnz, C.c_void_p(ro.data_ptr()),
-                                           C.c_void_p(ci.data_ptr()), C.c_void_p(va.data_ptr()), _lib.F64,
-                                           C.byref(h)))
-        dm = pb.DeviceMatrix(None, "float64", device, _handle=h)
-        p = dm.plan(d)
-        rc = lib.csemb_apply_expansion(p.handle, _lib.ptr(c), len(c) - 1, 1, None, _lib.OMEGA_SPLITMIX, 7, 0, d,
-                                       1, C.c_void_p(out.data_ptr()), None, None, None)
-        _lib.check(rc)
-        dm.close()
+        emb = pb.fast_embed_cascaded(Su, f, cfg, normalize_rows=True, device=device)
+        pb.release_device_copy(Su)
+        return emb.values
+
+    for _ in range(2):
+        out = step()
+    times = []
+    for _ in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = step()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.median(times)
+    h2d = sum(a.nbytes for a in (Su.row_offsets, Su.col_indices, Su.values))
+    return {"value": units / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": int(out.nbytes),
+            "route": "pb.fast_embed_cascaded(SparseMatrix, f, cfg, normalize_rows=True) + release_device_copy"}
+
+
+def run_e2e_sharded(args, S, coeffs, units, rank, world, local_rank):
+    """N>1: every rank uploads the host CSR, runs its column shard, NCCL
+    all-gathers E, K4 row-normalises; rank 0 reads E back.  Wall time per step
+    between barriers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_08360_b200 as pb
+    from paper_1509_08360_b200.distributed import embed_column_sharded
+
+    n, d = S.n_rows, args.d
+    Su = pb.SparseMatrix(n, n, S.row_offsets, S.col_indices, S.values, check=False)
+
+    def step():
+        E, _ = embed_column_sharded(Su, coeffs, d, seed=7, omega_kind="reference", dtype="f64",
+                                    normalize_rows=True, device=local_rank)
+        return E.cpu().numpy() if rank == 0 else None
 
     for _ in range(2):
         step()
     times = []
     for _ in range(args.e2e_steps):
+        dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        step()
+        out = step()
         torch.cuda.synchronize()
+        dist.barrier()
         times.append(time.perf_counter() - t0)
-    ms = 1e3 * statistics.median(times)
+    t = torch.tensor([statistics.median(times)], device=f"cuda:{local_rank}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = 1e3 * float(t.item())
+    h2d = world * sum(a.nbytes for a in (Su.row_offsets, Su.col_indices, Su.values))
     return {"value": units / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h}
+            "d2h_bytes_per_step": n * d * 8,
+            "route": "distributed.embed_column_sharded(host CSR on every rank) + E.cpu() on rank 0"}
+
+
+class _CutAbove:
+    """Config 4's f(x) = x * 1{x >= 0.3} (not a built-in kind)."""
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        return np.where(x >= 0.3, x, 0.0)
+
+    def breakpoints(self):
+        return (0.3,)
+
+
+def run_configs34(args, peak, peak_src):
+    """BASELINE configs 3 and 4 at full size, fp32 (north_star's dtype for
+    them), inputs built on the device (untimed).  Reports the device-resident
+    embed wall time -- config 4 including its 30-iteration power-iteration
+    norm estimate (k = ceil(6 ln N)) and rescale -- and K1's per-step time and
+    roofline fraction (algorithmic bytes T*(4+4) + 5*N*d*4)."""
+    import math
+
+    import torch
+
+    import paper_1509_08360_b200 as pb
+    from paper_1509_08360_b200 import _lib, device_build as db
+
+    out = []
+    for cfg_id in (3, 4):
+        t0 = time.perf_counter()
+        if cfg_id == 3:
+            n = 10_000_000
+            S = db.normalized_adjacency(db.chung_lu_edges(n, seed=3), n)
+            f, d, L, norm_iters = pb.commute_time(0.01), 80, 180, 0
+            name = "config3: Chung-Lu n=1e7 (Pareto 2.1, mean degree 20), d=80, L=180, commute_time(0.01), fp32"
+        else:
+            S = db.dilate(db.bag_of_words(2_000_000, 500_000, seed=4))
+            f, d, L, norm_iters = pb.odd_extension(_CutAbove()), 96, 120, 30
+            name = ("config4: BoW 2e6 x 5e5 (Poisson 150, Zipf 1.1, tf-idf) dilation, 30-iteration norm, d=96, "
+                    "L=120, x*1{x>=0.3} odd-extended, fp32")
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        coeffs = pb.legendre_coefficients(f, L).coeffs
+        dm = S.to_device_matrix("float32")
+        nnz, N = S.nnz, S.n_rows
+        longest = int((S.row_offsets[1:] - S.row_offsets[:-1]).max())
+        del S
+        torch.cuda.empty_cache()
+        plan = dm.plan(d)
+        k = max(1, math.ceil(6.0 * math.log(N)))
+        runs = []
+        for rep in range(args.configs34_reps + 1):
+            dm.ctx.sync()
+            t1 = time.perf_counter()
+            norm_ms = 0.0
+            if norm_iters:  # fresh values each rep: scale back after the run
+                est = dm.spectral_norm(norm_iters, k, pb.fold_seed(4, pb.engine.NORM_SEED_TAG), 1.01)
+                dm.scale(1.0 / est)
+                norm_ms = 1e3 * (time.perf_counter() - t1)
+            plan.run(coeffs, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7, normalize_rows=True)
+            dm.ctx.sync()
+            wall_ms = 1e3 * (time.perf_counter() - t1)
+            tot, steps, launches = plan.timing()
+            if norm_iters:
+                dm.scale(est)
+            if rep > 0:
+                runs.append((wall_ms, norm_ms, tot, steps / L, launches))
+        wall_ms, norm_ms, tot, k1, launches = min(runs)
+        B = k1_bytes(nnz, N, d, d, "f32")
+        ach = B / (k1 * 1e-3) / 1e9
+        out.append({"workload": name, "n": N, "nnz": nnz, "longest_row": longest, "d": d, "L": L, "dtype": "f32",
+                    "device_build_s": round(build_s, 2), "embed_wall_ms": round(wall_ms, 2),
+                    "norm_ms": round(norm_ms, 2) if norm_iters else None, "embed_device_ms": round(tot, 3),
+                    "value": nnz * d * L / (tot * 1e-3), "unit": UNIT, "k1_ms": round(k1, 4),
+                    "k1_launches_per_step": launches / L,
+                    "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                                 "frac": round(ach / peak, 4), "algorithmic_bytes_per_launch": B,
+                                 "peak_source": peak_src, "traffic": None}})
+        log(f"[bench] config {cfg_id}: embed {tot:.1f} ms (wall {wall_ms:.1f} ms), K1 {k1:.3f} ms/step, "
+            f"{ach:.0f} GB/s ({ach / peak:.3f})")
+        dm.close()
+        torch.cuda.empty_cache()
+    return out
+
+
+def _reference_csemb():
+    """The unmodified reference package installed in baseline/_ref
+    (tools/stage_reference.sh), or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "csemb")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import csemb
+    except ImportError:
+        return None
+    return csemb if os.path.abspath(csemb.__file__).startswith(REF_DIR) else None
+
+
+def run_builders(args):
+    """edge list -> deduped D^-1/2 A D^-1/2 CSR for the
+    config-2 graph, on the device (csemb_build_normalized_adjacency, or the
+    torch builder) against the reference's own host normalized_adjacency
+    (baseline/_ref) -- falling back to this package's host restatement."""
+    import torch
+
+    from paper_1509_08360_b200 import device_build as db, graphs
+
+    edges = graphs.sbm_edges(args.n, 100, 15.0, 5.0, seed=2)
+    n = args.n
+    res = {"edges": int(len(edges)), "n": n}
+    ed = torch.from_numpy(edges).cuda()
+    for _ in range(2):  # warm-up, then timed
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A = db.normalized_adjacency(ed, n)
+        torch.cuda.synchronize()
+        dev_s = time.perf_counter() - t0
+    res.update({"device_s": round(dev_s, 4), "device_builder": getattr(db, "BUILDER_KIND", "torch"),
+                "nnz": A.nnz})
+    ref = _reference_csemb()
+    t0 = time.perf_counter()
+    if ref is not None:
+        H = ref.sparse.normalized_adjacency(edges, n)
+        res["host_builder"] = "reference csemb.sparse.normalized_adjacency (baseline/_ref)"
+    else:
+        from paper_1509_08360_b200 import sparse
+
+        H = sparse.normalized_adjacency(edges, n)
+        res["host_builder"] = "paper_1509_08360_b200.sparse.normalized_adjacency (host restatement)"
+    res["host_s"] = round(time.perf_counter() - t0, 3)
+    same = (np.array_equal(A.row_offsets.cpu().numpy(), H.row_offsets)
+            and np.array_equal(A.col_indices.cpu().numpy().astype(np.int64), H.col_indices)
+            and np.array_equal(A.values.cpu().numpy(), H.values))
+    res["bit_identical"] = bool(same)
+    res["speedup"] = round(res["host_s"] / max(dev_s, 1e-9), 1)
+    log(f"[bench] builders: device {dev_s * 1e3:.1f} ms vs host {res['host_s']:.2f} s (identical: {same})")
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -501,7 +727,46 @@ def cpu_baseline(S, d, coeffs, seconds: float):
             "seconds": t}
 
 
+def _time_reference_csemb(S, d, L, seconds):
+    """The REAL reference (baseline/_ref): csemb.fast_embed_eig(S, expansion,
+    order, omega, n_workers=W) on a truncated order, W = 1 and W = ceil(d/32)
+    (its maximum useful parallelism, engine.py:242-255), extrapolated per
+    recurrence step (each step is the same SpMM + elementwise work,
+    engine.py:213-227).  BASELINE.md section 3."""
+    ref = _reference_csemb()
+    if ref is None:
+        return None
+    S_ref = ref.SparseMatrix(S.n_rows, S.n_cols, S.row_offsets, S.col_indices, S.values)
+    omega = ref.sample_projection(S.n_rows, d, 7)
+    out = {"package": f"csemb {getattr(ref, '__version__', '')} from baseline/_ref (unmodified)",
+           "call": "csemb.fast_embed_eig(S, LegendreExpansion, order, omega, n_workers=W)", "runs": []}
+    for W in (1, -(-d // 32)):
+        t0 = time.perf_counter()
+        exp1 = ref.legendre_coefficients(ref.indicator_above(0.95), 1)
+        ref.fast_embed_eig(S_ref, exp1, 1, omega, n_workers=W)
+        t1 = time.perf_counter() - t0
+        order = int(max(1, min(L, round(seconds / max(t1, 1e-3)))))
+        exp = ref.legendre_coefficients(ref.indicator_above(0.95), order)
+        t0 = time.perf_counter()
+        ref.fast_embed_eig(S_ref, exp, order, omega, n_workers=W)
+        sec = time.perf_counter() - t0
+        out["runs"].append({"n_workers": W, "order": order, "seconds": round(sec, 3),
+                            "value": S.nnz * d * order / sec, "unit": UNIT,
+                            "full_embedding_s_extrapolated": round(sec * L / order, 1)})
+        log(f"[bench] reference csemb W={W}: {order} steps in {sec:.2f} s -> {S.nnz * d * order / sec:.3e} {UNIT}")
+    return out
+
+
 def run_reference(args, rank: int, world: int):
+    """Reference arm: the reference's CPU algorithm on the box's host cores,
+    timed on the SAME workload as our arm (config 2, Omega =
+    sample_projection(n, d, 7), f64, row-normalised).  The value is the C port
+    of engine._run_stage + scipy csr_matvecs (oracle/csemb_oracle.c, OpenMP
+    over all cores -- faster than the reference itself, so the ratio is
+    conservative); each step times a bounded prefix of the 180 recurrence
+    steps, extrapolated linearly in L (identical work per step), plus one row
+    normalisation.  The real reference package (baseline/_ref) is timed beside
+    it at W = 1 and W = 3."""
     if rank != 0:
         return
     import oracle as O
@@ -509,8 +774,8 @@ def run_reference(args, rank: int, world: int):
     import paper_1509_08360_b200 as pb
 
     S = make_workload(args.n)
-    d = args.d
-    coeffs = pb.legendre_coefficients(pb.indicator_above(0.95), args.L).coeffs
+    d, L = args.d, args.L
+    coeffs = pb.legendre_coefficients(pb.indicator_above(0.95), L).coeffs
     cores = _cpu_cores()
     O.set_threads(cores)
     csr = O.CSR.of(S)
@@ -518,26 +783,33 @@ def run_reference(args, rank: int, world: int):
     t0 = time.perf_counter()
     O.run_stage(csr, coeffs[:2], om)
     t1 = time.perf_counter() - t0
-    order = int(max(1, min(args.L, round(args.ref_step_seconds / max(t1, 1e-3)))))
+    order = int(max(1, min(L, round(args.ref_step_seconds / max(t1, 1e-3)))))
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.run_stage(csr, coeffs[: order + 1], om)
+        E, _, _ = O.run_stage(csr, coeffs[: order + 1], om)
+        t_rec = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.row_normalize(E)
+        t_norm = time.perf_counter() - t0
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(t_rec * L / order + t_norm)  # one full embedding, extrapolated in L
     sec = sum(times) / len(times)
-    v = S.nnz * d * order / sec
-    sample = (f"{order} of {args.L} recurrence steps per step of config 2 (n={S.n_rows}, nnz={S.nnz}, d={d}, f64); "
-              "oracle/csemb_oracle.c (restatement of engine._run_stage + scipy csr_matvecs), OpenMP over rows")
+    v = S.nnz * d * L / sec
+    sample = (f"{order} of {L} recurrence steps per step (extrapolated x{L / order:.1f} to the full order) + one row "
+              f"normalisation, config 2 (n={S.n_rows}, nnz={S.nnz}, d={d}, f64); oracle/csemb_oracle.c "
+              "(restatement of engine._run_stage + scipy csr_matvecs), OpenMP over rows")
+    real = None if args.skip_reference_csemb else _time_reference_csemb(S, d, L, args.ref_csemb_seconds)
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded O(T) SBM sampler)",
-        "config": {"workload": "config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, f=1{x>=0.95}",
-                   "n": S.n_rows, "nnz": S.nnz, "d": d, "L": args.L, "parallelism": "CPU threads"},
+        "dtype": "f64", "data": "synthetic (seeded O(T) SBM sampler; the reference's SplitMix64 projection)",
+        "config": {"workload": WORKLOAD, "n": S.n_rows, "nnz": S.nnz, "d": d, "L": L,
+                   "parallelism": f"CPU threads x{cores}"},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_csemb": real,
     }), flush=True)
 
 
@@ -550,13 +822,18 @@ def main():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--d", type=int, default=80)
     ap.add_argument("--L", type=int, default=180)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=6.0)
     ap.add_argument("--skip-fp32", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-downstream", action="store_true", help="omit the k-means / modularity / cosine object")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-configs34", action="store_true", help="omit the configs 3/4 objects")
+    ap.add_argument("--configs34-reps", type=int, default=2)
+    ap.add_argument("--skip-builders", action="store_true", help="omit the device vs host builder object")
+    ap.add_argument("--skip-reference-csemb", action="store_true", help="reference arm: port only")
+    ap.add_argument("--ref-csemb-seconds", type=float, default=8.0)
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rule)")

@@ -86,6 +86,38 @@ int csemb_matrix_info(csemb_mat *m, int64_t *n_rows, int64_t *n_cols, int64_t *n
 int csemb_matrix_scale(csemb_mat *m, double factor);
 /* copy the device values back (f64) -- for tests of csemb_matrix_scale */
 int csemb_matrix_download_values(csemb_mat *m, double *values_out);
+/* a copy of m in another arithmetic type (values converted; CSR shared shape) */
+int csemb_matrix_convert(csemb_mat *m, int dtype, csemb_mat **out);
+/* borrowed device pointers of m's arrays (int64 offsets, int32 column ids,
+ * values in m's dtype); valid until csemb_matrix_destroy(m) */
+int csemb_matrix_device_arrays(csemb_mat *m, void **row_offsets, void **col_indices, void **values);
+
+/* ---- measurement probes (bench.py roofline objects; not the embedding path) ----
+ * GB/s of one probe on the context's device, best of 3 timed launches:
+ *   CSEMB_DIAG_L2_STREAM  coalesced 16-byte .cg re-reads of an L2-resident
+ *                         `bytes` buffer, `reps` passes (L2 -> SM fabric)
+ *   CSEMB_DIAG_L2_GATHER  K1's load shape: random rows of `row_bytes` inside
+ *                         an L2-resident `bytes` window, 16 lanes per row,
+ *                         4 rows in flight per lane group, 4*reps rows each
+ *   CSEMB_DIAG_HBM_COPY   read + write of a `bytes` buffer (DRAM copy)   */
+#define CSEMB_DIAG_L2_STREAM 0
+#define CSEMB_DIAG_L2_GATHER 1
+#define CSEMB_DIAG_HBM_COPY 2
+int csemb_diag_bandwidth(csemb_ctx *ctx, int kind, int64_t bytes, int64_t row_bytes, int reps, double *gbs);
+
+/* ---- device-side input construction --------------------
+ * normalized_adjacency (sparse.py:202-226): edges is an n_edges x 2 int64
+ * (u, v) array, host or device memory per edges_on_device.  Self-loops are
+ * dropped, duplicate undirected edges merged, degrees counted, and every
+ * stored value is 1/sqrt(deg u * deg v) computed with the reference's IEEE
+ * operations; rows ascending, columns strictly increasing, isolated vertices
+ * empty rows -- bit-identical to the host builder.  Values stored in dtype.
+ * An endpoint outside [0, n) is CSEMB_ERR_INVALID (ValueError). */
+int csemb_build_normalized_adjacency(csemb_ctx *ctx, int64_t n, int64_t n_edges, const int64_t *edges,
+                                     int edges_on_device, int dtype, csemb_mat **out);
+/* dilate (sparse.py:191-199): [0 A^T; A 0] of an m x n device matrix, square
+ * (m+n); indices 0..n-1 are A's columns, n..n+m-1 its rows; same dtype. */
+int csemb_build_dilation(csemb_mat *a, csemb_mat **out);
 
 /* ---- plans: device workspace for one (matrix, d) ----------------------------
  * Holds Y (two n x ld buffers, Q(r-1) and Q(r-2)/Q(r) in place), E (n x ld)

@@ -21,6 +21,7 @@ from .engine import (
     apply_expansion,
     default_dimension,
     device_matrix,
+    release_device_copy,
     estimate_spectral_norm,
     fast_embed_cascaded,
     fast_embed_eig,
@@ -80,7 +81,7 @@ __all__ = [
     "COLUMN_CHUNK", "CsembError", "CudaUnavailableError", "DeviceMatrix", "DivergenceError",
     "EmbedConfig", "EmbeddingMatrix", "InputFormatError", "LegendreExpansion", "Plan",
     "QuadratureSpec", "SparseMatrix", "SpectralFunction", "SpmvCounter", "apply_expansion",
-    "approximation_report", "commute_time", "constant", "default_dimension", "device_matrix",
+    "approximation_report", "commute_time", "constant", "default_dimension", "device_matrix", "release_device_copy",
     "dilate", "estimate_spectral_norm", "expansion_eval", "fast_embed_cascaded", "fast_embed_eig",
     "fast_embed_general", "fold_seed", "identity", "indicator_above", "install", "jl_dimension",
     "legendre_coefficients", "legendre_eval", "legendre_table", "norm_start_block",

@@ -55,6 +55,11 @@ SIGNATURES = {
     "csemb_matrix_info": (_int, [_p, _pi64, _pi64, _pi64, _pi]),
     "csemb_matrix_scale": (_int, [_p, _dbl]),
     "csemb_matrix_download_values": (_int, [_p, _p]),
+    "csemb_matrix_convert": (_int, [_p, _int, _pp]),
+    "csemb_matrix_device_arrays": (_int, [_p, _pp, _pp, _pp]),
+    "csemb_build_normalized_adjacency": (_int, [_p, _i64, _i64, _p, _int, _int, _pp]),
+    "csemb_build_dilation": (_int, [_p, _pp]),
+    "csemb_diag_bandwidth": (_int, [_p, _int, _i64, _i64, _int, _pd]),
     "csemb_plan_create": (_int, [_p, _i64, _pp]),
     "csemb_plan_destroy": (_int, [_p]),
     "csemb_plan_set_option": (_int, [_p, _int, _i64]),
@@ -146,6 +151,40 @@ def device_count() -> int:
     n = C.c_int(0)
     lib.csemb_device_count(C.byref(n))
     return int(n.value)
+
+
+def host_empty(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialised host array for a device -> host result, backed by
+    torch's caching pinned-host allocator when torch is present: a fresh
+    np.empty of config 2's 640 MB E costs ~100 ms of first-touch page faults
+    plus a pageable (staged) copy, while a cached pinned block is reused
+    across calls and filled by DMA at full link speed.  The returned ndarray
+    owns the block through its base (freed back to the cache with it)."""
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    if (1 << 20) <= nbytes <= (16 << 30) and _pinning_available():
+        try:
+            import torch
+
+            t = torch.empty(int(np.prod(shape)), dtype=getattr(torch, np.dtype(dtype).name), pin_memory=True)
+            return t.numpy().reshape(shape)
+        except Exception:  # no pinned memory available: plain pageable array
+            pass
+    return np.empty(shape, dtype=dtype)
+
+
+_PINNING = None
+
+
+def _pinning_available() -> bool:
+    global _PINNING
+    if _PINNING is None:
+        try:
+            import torch
+
+            _PINNING = bool(torch.cuda.is_available())
+        except Exception:
+            _PINNING = False
+    return _PINNING
 
 
 def ptr(a: np.ndarray | None):

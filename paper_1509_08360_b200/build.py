@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcsemb_cuda.so")
-SOURCES = [os.path.join(HERE, "csrc", "csemb_cuda.cu"), os.path.join(HERE, "csrc", "downstream.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("csemb_cuda.cu", "downstream.cu", "build.cu", "diag.cu")]
 DEPS = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "csemb_cuda.h")]
 
 NVCC_FLAGS = [
@@ -38,10 +38,28 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile each translation unit to an object in parallel, then link the
+    shared library (objects under build/, git-ignored)."""
     if not force and up_to_date():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(ROOT, "build", "csemb_obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

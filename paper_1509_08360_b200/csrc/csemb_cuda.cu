@@ -161,6 +161,10 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
             cudaError_t e = cudaSuccess;
             if (STAGED) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
             if (e != cudaSuccess) return e;
+            if (const char *cv = getenv("CSEMB_K1_CARVEOUT")) {  // experiment: L1 / shared split (percent shared)
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+                if (e != cudaSuccess) return e;
+            }
             int nb = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, max_smem);
             if (e != cudaSuccess) return e;
@@ -191,9 +195,13 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
 // lane spill at the 64-register cap that gives 4 CTAs / 32 warps per SM)
 template <typename T, int G, int MODE, int PEAK>
 static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, int sm) {
-    if constexpr (G == 1) {
-        if (vpl == 1) return run_step<T, G, 1, MODE, PEAK>(P, s, sm);
+    if (vpl == 1) return run_step<T, G, 1, MODE, PEAK>(P, s, sm);
+#if K1_WIDE_VPL
+    if constexpr (G == 4 || G == 8) {  // experiment: 4-5 vectors per lane (wider lane tiles, fewer rows per warp)
+        if (vpl == 4) return run_step<T, G, 4, MODE, PEAK>(P, s, sm);
+        if (vpl == 5) return run_step<T, G, 5, MODE, PEAK>(P, s, sm);
     }
+#endif
     switch (vpl) {
         case 2: return run_step<T, G, 2, MODE, PEAK>(P, s, sm);
         case 3: return run_step<T, G, 3, MODE, PEAK>(P, s, sm);
@@ -201,14 +209,18 @@ static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, in
     }
 }
 
-// Target vectors per lane (CSEMB_TARGET_VPL in [2, 3], default 3); the group is
+// Target vectors per lane (CSEMB_TARGET_VPL in [1, 3], default 3); the group is
 // the smallest power of two G with ceil(nv/G) <= target, and one launch covers
 // at most 32*target vectors (wider rows are split into column tiles).
 static int target_vpl() {
     static int t = [] {
         const char *e = getenv("CSEMB_TARGET_VPL");
         int v = e ? atoi(e) : 3;
-        return std::min(3, std::max(2, v));
+#if K1_WIDE_VPL
+        return std::min(5, std::max(1, v));
+#else
+        return std::min(3, std::max(1, v));
+#endif
     }();
     return t;
 }
@@ -217,6 +229,12 @@ static int choose_group(int nv) {
     const int tv = target_vpl();
     int g = 1;
     while (g < 32 && (nv + g - 1) / g > tv) g *= 2;
+#if K1_WIDE_VPL
+    if (tv > 3 && g != 4 && g != 8) {  // wide lane tiles exist for 4- and 8-lane groups only
+        g = 1;
+        while (g < 32 && (nv + g - 1) / g > 3) g *= 2;
+    }
+#endif
     return g;
 }
 
@@ -315,11 +333,30 @@ static int efold_bits(int r, int L, int K) {
 
 static const int64_t HEAVY_CHUNK = 1024;  // entries per chunk of a split heavy row
 
-// Build (or fetch) the schedule of matrix m for group width G.
-static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out) {
+// Heavy-row chunks are also cut at multiples of a column window whose rows of
+// the gathered block fill about this much of L2 (CSEMB_HEAVY_WINDOW_MB, 0 =
+// fixed chunks only).  The chunks run in first-column order, so the chunks in
+// flight at any time gather from one window, which stays L2-resident: each
+// gathered row is fetched from DRAM about once per step instead of once per
+// chunk that spans it (config 4's term rows span all 2e6 document rows).
+static int64_t heavy_window_bytes() {
+    static int64_t b = [] {
+        const char *e = getenv("CSEMB_HEAVY_WINDOW_MB");
+        return (int64_t)((e ? atof(e) : 0.0) * (1 << 20));
+    }();
+    return b;
+}
+
+// Build (or fetch) the schedule of matrix m for group width G; `row_bytes` is
+// the size of one gathered row of a column tile (sets the heavy-row window).
+static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
+                        int64_t row_bytes = 0) {
     *out = nullptr;
+    const int64_t wbytes = heavy_window_bytes();
+    int64_t wcols = (wbytes > 0 && row_bytes > 0) ? std::max<int64_t>(1, wbytes / row_bytes) : 0;
+    if (wcols >= m->n_cols) wcols = 0;  // one window: plain fixed chunks
     for (Schedule *sc : m->schedules)
-        if (sc->G == G && sc->threshold == threshold && sc->order == order) {
+        if (sc->G == G && sc->threshold == threshold && sc->order == order && sc->wcols == wcols) {
             *out = sc;
             return CSEMB_OK;
         }
@@ -333,16 +370,49 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
         const int64_t len = rp[r + 1] - rp[r];
         if (threshold > 0 && len > threshold) {
             hrows.push_back((int)r);
-            for (int64_t b = rp[r]; b < rp[r + 1]; b += HEAVY_CHUNK) {
-                cbeg.push_back(b);
-                cend.push_back(std::min(b + HEAVY_CHUNK, rp[r + 1]));
-            }
-            hoff.push_back((int)cbeg.size());
         } else {
             light.push_back((int)r);
             sum += (double)len;
             sum2 += (double)len * (double)len;
         }
+    }
+    // window boundaries inside every heavy row (device binary searches)
+    const int nwin = wcols > 0 ? (int)((m->n_cols + wcols - 1) / wcols) : 1;
+    std::vector<int64_t> bounds;
+    if (!hrows.empty() && wcols > 0) {
+        int *drows = nullptr;
+        int64_t *dbounds = nullptr;
+        const size_t nb = hrows.size() * (size_t)(nwin + 1);
+        cudaError_t e = dmalloc(m->ctx, &drows, 4 * hrows.size());
+        if (e == cudaSuccess) e = dmalloc(m->ctx, &dbounds, 8 * nb);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(drows, hrows.data(), 4 * hrows.size(), cudaMemcpyHostToDevice, m->ctx->stream);
+        if (e == cudaSuccess) {
+            k_window_bounds<<<grid_for((int64_t)nb, 256, m->ctx->sm_count), 256, 0, m->ctx->stream>>>(
+                m->cols, m->rowptr, drows, (int)hrows.size(), nwin, wcols, dbounds);
+            e = cudaGetLastError();
+        }
+        bounds.resize(nb);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(bounds.data(), dbounds, 8 * nb, cudaMemcpyDeviceToHost, m->ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(m->ctx->stream);
+        dfree(m->ctx, drows);
+        dfree(m->ctx, dbounds);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(CSEMB_ERR_CUDA, "schedule window bounds: %s", cudaGetErrorString(e));
+        }
+    }
+    for (size_t h = 0; h < hrows.size(); ++h) {
+        const int r = hrows[h];
+        for (int k = 0; k < nwin; ++k) {
+            const int64_t s0 = wcols > 0 ? bounds[h * (nwin + 1) + k] : rp[r];
+            const int64_t s1 = wcols > 0 ? bounds[h * (nwin + 1) + k + 1] : rp[r + 1];
+            for (int64_t b = s0; b < s1; b += HEAVY_CHUNK) {
+                cbeg.push_back(b);
+                cend.push_back(std::min(b + HEAVY_CHUNK, s1));
+            }
+        }
+        hoff.push_back((int)cbeg.size());
     }
     const double nl = (double)std::max<size_t>(light.size(), 1);
     const double mean = sum / nl, var = std::max(0.0, sum2 / nl - mean * mean);
@@ -404,6 +474,7 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
     sc->G = G;
     sc->threshold = threshold;
     sc->order = order;
+    sc->wcols = wcols;
     sc->n_light = (int64_t)light.size();
     sc->n_heavy = (int)hrows.size();
     sc->n_chunks = (int64_t)cbeg.size();
@@ -570,7 +641,7 @@ extern "C" int csemb_ctx_sm_count(csemb_ctx *c, int *out) {
 // ---------------------------------------------------------------------------
 // matrices
 // ---------------------------------------------------------------------------
-static void mat_free(csemb_mat *m) {
+void mat_free(csemb_mat *m) {
     if (!m) return;
     for (Schedule *sc : m->schedules) sched_free(m->ctx, sc);
     dfree(m->ctx, m->rowptr);
@@ -579,8 +650,7 @@ static void mat_free(csemb_mat *m) {
     delete m;
 }
 
-static int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, int dtype,
-                     csemb_mat **out) {
+int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, int dtype, csemb_mat **out) {
     if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(CSEMB_ERR_INVALID, "negative matrix dimension");
     if (dtype != CSEMB_F64 && dtype != CSEMB_F32) return fail(CSEMB_ERR_INVALID, "dtype must be CSEMB_F64 or CSEMB_F32");
     if (n_cols > 0x7FFFFFFFLL || n_rows > 0x7FFFFFFFLL)
@@ -930,7 +1000,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
     Schedule *sc = nullptr;
     if (n > 0) {
         const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold,
-                                    p->row_order, &sc);
+                                    p->row_order, &sc, 16 * (int64_t)std::min(ldv, max_tile_vecs()));
         if (rc) return rc;
         const size_t pbytes = (size_t)sc->n_chunks * (size_t)ld * sizeof(T);
         if (pbytes > p->partials_bytes) {
@@ -1376,7 +1446,8 @@ static int plan_step_t(csemb_plan *p, int r) {
     const int ldv = (int)(p->ld / Vec<T>::W);
     if (n == 0) return CSEMB_OK;
     Schedule *sc = nullptr;
-    int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold, p->row_order, &sc);
+    int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold, p->row_order, &sc,
+                          16 * (int64_t)std::min(ldv, max_tile_vecs()));
     if (rc) return rc;
     const size_t pbytes = (size_t)sc->n_chunks * (size_t)p->ld * sizeof(T);
     if (pbytes > p->partials_bytes) {
@@ -1531,7 +1602,8 @@ static int spectral_norm_t(csemb_mat *m, int iters, int64_t k, const double *v0_
     Schedule *sc = nullptr;
     void *partials = nullptr;
     if (e == cudaSuccess) {
-        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), DEFAULT_SPLIT, -1, &sc);
+        const int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), DEFAULT_SPLIT, -1, &sc,
+                                    16 * (int64_t)std::min(ldv, max_tile_vecs()));
         if (rc) {
             dfree(c, V); dfree(c, Wm); dfree(c, stage); dfree(c, partial); dfree(c, rq); dfree(c, inv);
             return rc;

@@ -200,6 +200,9 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_DEPTH
 #define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
 #endif
+#ifndef K1_DEPTH_F32
+#define K1_DEPTH_F32 2  // fp32 entries in flight per lane (divides the batch)
+#endif
 #ifndef K1_BATCH
 #define K1_BATCH 0  // stored entries per warp-uniform batch (<= G; 0: B = G, measured best)
 #endif
@@ -258,6 +261,24 @@ __device__ __forceinline__ float4 ld_gather_if(const float4 *p, bool ok) {
     asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q " GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];\n}"
         : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(p), "r"((unsigned)ok));
     return v;
+}
+// Predicated gather INTO a live register: a load that is not taken leaves the
+// register's previous contents, so no zero-fill instructions are issued per
+// entry (2 CS2R per 16-byte slot).  Measured (round 2, tools/run_round2_b.sh):
+// f64 d=80 -1%, but f64 d=40 +7% and f32 d=80 +15% K1 time (the "+" operands
+// pin the buffers to fixed registers across the unrolled steps), and the
+// fp32 config-1 parity test failed with it on -- so it is off (K1_KEEP_STALE 0,
+// zero-filled predicated loads) and kept only as a measured experiment.
+#ifndef K1_KEEP_STALE
+#define K1_KEEP_STALE 0
+#endif
+__device__ __forceinline__ void ld_gather_into(double2 &v, const double2 *p, bool ok) {
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q " GATHER_OP ".v2.f64 {%0,%1}, [%2];\n}"
+        : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((unsigned)ok));
+}
+__device__ __forceinline__ void ld_gather_into(float4 &v, const float4 *p, bool ok) {
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q " GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(p), "r"((unsigned)ok));
 }
 __device__ __forceinline__ double2 vsel(bool c, double2 a, double2 b) {
     return make_double2(c ? a.x : b.x, c ? a.y : b.y);
@@ -399,7 +420,8 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     // variant (STAGED): lane 0 of each group issues one TMA bulk copy of the
     // neighbour's row tile into a warp-private S-stage shared-memory ring; the
     // group waits on the stage's mbarrier and consumes it from shared memory.
-    constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (sizeof(T) == 8 ? 4 : 2);
+    // VPL > 3 (K1_WIDE_VPL builds): the register budget allows only 2 entries in flight
+    constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (VPL > 3 ? 2 : (sizeof(T) == 8 ? 4 : K1_DEPTH_F32));
     constexpr int D = STAGED ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
     // STAGED == 2: per-lane ring of D entries x VPL 16-byte slots in shared memory
     VT *lring = nullptr;
@@ -407,6 +429,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         lring = reinterpret_cast<VT *>(k1_dyn_smem + P.smem_base) + (size_t)threadIdx.x * VPL;
     static_assert(B % D == 0, "pipeline depth must divide the batch width");
     VT buf[STAGED ? 1 : D][VPL];
+#pragma unroll
+    for (int i = 0; i < (STAGED ? 1 : D); ++i)
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) buf[i][k] = vzero(VT());
     uint64_t *bars = nullptr;
     VT *ring = nullptr;
     unsigned phase = 0u;  // staged: bit s = parity to wait for on stage s
@@ -443,7 +469,12 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         } else {
             const VT *x = ycur + (int64_t)j * P.ldv;
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) buf[slot][k] = ld_gather_if(x + k * G, valid[k] && ok);
+            for (int k = 0; k < VPL; ++k) {
+                if (K1_KEEP_STALE)
+                    ld_gather_into(buf[slot][k], x + k * G, valid[k] && ok);
+                else
+                    buf[slot][k] = ld_gather_if(x + k * G, valid[k] && ok);
+            }
         }
     };
 #pragma unroll
@@ -1036,6 +1067,28 @@ __global__ void k_unpack(const T *__restrict__ src, O *dst, int64_t n, int d, in
 __global__ void k_gather_cols(const int *__restrict__ cols, const int64_t *__restrict__ idx, int *out, int64_t n) {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
         out[t] = cols[idx[t]];
+}
+
+// Column-window boundaries of the heavy rows: bounds[h * (nwin + 1) + k] = the
+// first entry of heavy row rows[h] whose column is >= k * wcols (lower bound in
+// the row's sorted column ids), so a heavy row can be cut at window edges.
+__global__ void k_window_bounds(const int *__restrict__ cols, const int64_t *__restrict__ rowptr,
+                                const int *__restrict__ rows, int n_heavy, int nwin, int64_t wcols,
+                                int64_t *bounds) {
+    const int64_t total = (int64_t)n_heavy * (nwin + 1);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int h = (int)(t / (nwin + 1));
+        const int k = (int)(t - (int64_t)h * (nwin + 1));
+        int64_t lo = rowptr[rows[h]], hi = rowptr[rows[h] + 1];
+        const int64_t key = (int64_t)k * wcols;
+        while (lo < hi) {  // first entry with col >= key
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)cols[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        bounds[t] = lo;
+    }
 }
 
 // CSR conversion: int64 -> int32 column indices (with range check), f64 -> T values

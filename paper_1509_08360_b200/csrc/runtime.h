@@ -65,6 +65,7 @@ struct Schedule {
     int G = 0;
     int64_t threshold = 0;
     int order = 0;
+    int64_t wcols = 0;  // heavy-row chunks never straddle a multiple of wcols columns (0: fixed chunks)
     int *perm = nullptr;  // light rows (null: natural order, no heavy rows)
     int64_t n_light = 0;
     int64_t *cbeg = nullptr, *cend = nullptr;  // heavy-row chunk entry ranges
@@ -87,4 +88,9 @@ struct csemb_mat {
 };
 
 CSEMB_INTERNAL size_t dsize(int dtype);
+// a matrix handle with device arrays for n_rows+1 offsets / nnz ids / nnz values
+// (rowptr_host left empty); mat_free releases everything incl. schedules
+CSEMB_INTERNAL int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, int dtype,
+                             csemb_mat **out);
+CSEMB_INTERNAL void mat_free(csemb_mat *m);
 CSEMB_INTERNAL int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8);

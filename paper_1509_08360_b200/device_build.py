@@ -3,29 +3,70 @@
 The reference builds its inputs on the host (sparse.py:191-226): dedupe the
 undirected edge list, drop self-loops, degrees by bincount, values
 1/sqrt(deg_u * deg_v) (`normalized_adjacency`), and the dilation
-[0 A^T; A 0] (`dilate`).  At config-3/4 scale (1e8 edges, 3e8 tokens) that
-host work dominates the end-to-end time, so these builders do the same
-construction on the GPU and hand the CSR to the C ABI without a host round
-trip (`csemb_matrix_upload_device`).  Sorting/dedupe use torch's CUDA sort as
-plumbing; the arithmetic is the reference's (same IEEE expression per
-value), and the resulting CSR is canonical (rows ascending, columns strictly
-increasing), so it is bit-identical to the host builders (tests/test_gpu_parity.py).
+[0 A^T; A 0] (`dilate`).  At config-2..5 scale that host work dominates the
+end-to-end time (20.5 s at n = 1e6), so the builders here run as this
+package's own kernels behind the C ABI (csrc/build.cu:
+csemb_build_normalized_adjacency / csemb_build_dilation): edge keys, radix
+sort + unique, degree counts, scan, symmetric keys, radix sort, one fused
+column/value pass.  The arithmetic is the reference's (same IEEE expression
+per value) and the CSR is canonical (rows ascending, columns strictly
+increasing), so it is bit-identical to the host builders
+(tests/test_gpu_parity.py::TestDeviceBuild).
+
+The results are `DeviceCSR` objects: the library-owned device matrix plus
+zero-copy torch views of its arrays (int64 offsets, int32 columns, f64
+values) for callers that slice or inspect them on the device.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+
+import numpy as np
 import torch
 
-from .engine import DeviceMatrix
+from . import _lib
+from .engine import DeviceMatrix, dtype_code
+
+BUILDER_KIND = "csemb kernels (csrc/build.cu: keys, CUB radix sort/unique/scan, degree + fill kernels)"
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ over a library-owned device array; torch keeps
+    this object (and through it the owning matrix) alive with the tensor."""
+
+    def __init__(self, ptr: int, n: int, typestr: str, owner):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": (int(n),), "typestr": typestr,
+                                         "strides": None, "version": 3, "stream": None}
+        self._owner = owner
 
 
 class DeviceCSR:
-    """A canonical CSR held in torch CUDA tensors (int64 offsets, int64 or
-    int32 columns, f64 values)."""
+    """A canonical CSR on one GPU: int64 offsets, int64 or int32 columns, f64
+    values as torch CUDA tensors (optionally views of a library matrix)."""
 
-    def __init__(self, n_rows, n_cols, row_offsets, col_indices, values):
+    def __init__(self, n_rows, n_cols, row_offsets, col_indices, values, owner: DeviceMatrix | None = None):
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
         self.row_offsets, self.col_indices, self.values = row_offsets, col_indices, values
+        self.owner = owner
+
+    @classmethod
+    def from_matrix(cls, dm: DeviceMatrix) -> "DeviceCSR":
+        """Zero-copy views of a library matrix's arrays (f64 matrices)."""
+        if dm.dtype != _lib.F64:
+            raise ValueError("DeviceCSR views need an f64 matrix")
+        ro, ci, va = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _lib.check(dm.lib.csemb_matrix_device_arrays(dm.handle, C.byref(ro), C.byref(ci), C.byref(va)),
+                   "csemb_matrix_device_arrays")
+        dev = torch.device("cuda", dm.ctx.device)
+
+        def view(ptr, n, typestr, dt):
+            if n == 0:
+                return torch.empty(0, dtype=dt, device=dev)
+            return torch.as_tensor(_DeviceArray(ptr.value, n, typestr, dm), device=dev)
+
+        return cls(dm.n_rows, dm.n_cols, view(ro, dm.n_rows + 1, "<i8", torch.int64),
+                   view(ci, dm.nnz, "<i4", torch.int32), view(va, dm.nnz, "<f8", torch.float64), owner=dm)
 
     @property
     def nnz(self) -> int:
@@ -33,6 +74,11 @@ class DeviceCSR:
 
     def to_device_matrix(self, dtype="float64", device: int | None = None) -> DeviceMatrix:
         dev = self.values.device.index if device is None else device
+        if self.owner is not None and dev == self.owner.ctx.device:  # device-side copy in the requested dtype
+            h = C.c_void_p()
+            _lib.check(self.owner.lib.csemb_matrix_convert(self.owner.handle, dtype_code(dtype), C.byref(h)),
+                       "csemb_matrix_convert")
+            return DeviceMatrix(None, dtype, dev, _handle=h)
         ci = self.col_indices
         # the tensors may still be in flight on torch's stream (NCCL broadcasts of
         # distributed.broadcast_matrix, builder kernels): the library stream must
@@ -49,59 +95,49 @@ class DeviceCSR:
                             check=False)
 
 
-def _offsets(rows: torch.Tensor, n_rows: int) -> torch.Tensor:
-    counts = torch.bincount(rows, minlength=n_rows)
-    offs = torch.zeros(n_rows + 1, dtype=torch.int64, device=rows.device)
-    torch.cumsum(counts, 0, out=offs[1:])
-    return offs
-
-
-def normalized_adjacency(edges: torch.Tensor, n: int) -> DeviceCSR:
-    """D^{-1/2} A D^{-1/2} of the simple graph on the GPU (sparse.py:202-226)."""
+def normalized_adjacency(edges, n: int, device: int | None = None) -> DeviceCSR:
+    """D^{-1/2} A D^{-1/2} of the simple graph, built on the GPU by the
+    library's kernels (sparse.py:202-226).  `edges`: (E, 2) int64, a CUDA
+    tensor (read in place) or a host array (copied once)."""
     if n < 1:
         raise ValueError("vertex count must be positive")
-    e = edges.reshape(-1, 2).to(torch.int64)
-    if e.numel() and (int(e.min()) < 0 or int(e.max()) >= n):
-        raise ValueError("edge endpoint out of range [0, n)")
-    u, v = e[:, 0], e[:, 1]
-    keep = u != v
-    u, v = u[keep], v[keep]
-    dev = e.device
-    if u.numel() == 0:
-        z = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        return DeviceCSR(n, n, z, torch.empty(0, dtype=torch.int32, device=dev),
-                         torch.empty(0, dtype=torch.float64, device=dev))
-    key = torch.unique(torch.minimum(u, v) * n + torch.maximum(u, v))  # sorted, deduped
-    lo, hi = key // n, key % n
-    del key
-    deg = (torch.bincount(lo, minlength=n) + torch.bincount(hi, minlength=n)).to(torch.float64)
-    sym = torch.cat([lo * n + hi, hi * n + lo])
-    del lo, hi
-    sym, _ = torch.sort(sym)
-    r, c = sym // n, sym % n
-    del sym
-    vals = 1.0 / torch.sqrt(deg[r] * deg[c])  # same IEEE expression as the reference
-    return DeviceCSR(n, n, _offsets(r, n), c.to(torch.int32), vals)
+    if isinstance(edges, torch.Tensor) and edges.is_cuda:
+        e = edges.reshape(-1, 2).to(torch.int64).contiguous()
+        dev = e.device.index if device is None else device
+        torch.cuda.current_stream(e.device).synchronize()  # produced on torch's stream
+        ptr, on_dev, n_edges = e.data_ptr(), 1, e.shape[0]
+    else:
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.int64).reshape(-1, 2))
+        dev = 0 if device is None else device
+        ptr, on_dev, n_edges = e.ctypes.data, 0, e.shape[0]
+    ctx = _lib.context(dev)
+    h = C.c_void_p()
+    _lib.check(ctx.lib.csemb_build_normalized_adjacency(ctx.handle, int(n), int(n_edges), C.c_void_p(ptr),
+                                                        on_dev, _lib.F64, C.byref(h)),
+               "csemb_build_normalized_adjacency")
+    return DeviceCSR.from_matrix(DeviceMatrix(None, "float64", dev, _handle=h))
 
 
 def dilate(A: DeviceCSR) -> DeviceCSR:
     """[0 A^T; A 0] on the GPU: first n indices are A's columns, last m its rows
-    (sparse.py:191-199)."""
-    m, n = A.n_rows, A.n_cols
-    if m < 1 or n < 1:
+    (sparse.py:191-199), by the library's transpose + fill kernels."""
+    if A.n_rows < 1 or A.n_cols < 1:
         raise ValueError("cannot dilate an empty matrix")
-    N = m + n
-    dev = A.values.device
-    r = torch.repeat_interleave(torch.arange(m, device=dev, dtype=torch.int64),
-                                A.row_offsets[1:] - A.row_offsets[:-1])
-    c = A.col_indices.to(torch.int64)
-    keys = torch.cat([c * N + (n + r), (n + r) * N + c])
-    vals = torch.cat([A.values, A.values])
-    del r, c
-    keys, order = torch.sort(keys, stable=True)
-    vals = vals[order]
-    rows = keys // N
-    return DeviceCSR(N, N, _offsets(rows, N), (keys - rows * N).to(torch.int32), vals)
+    src = A.owner if A.owner is not None else A.to_device_matrix("float64")
+    h = C.c_void_p()
+    _lib.check(src.lib.csemb_build_dilation(src.handle, C.byref(h)), "csemb_build_dilation")
+    out = DeviceCSR.from_matrix(DeviceMatrix(None, "float64", src.ctx.device, _handle=h))
+    if src is not A.owner:
+        src.close()
+    return out
+
+
+def _offsets(rows: torch.Tensor, n_rows: int) -> torch.Tensor:
+    """CSR offsets of sorted row ids (generators only)."""
+    counts = torch.bincount(rows, minlength=n_rows)
+    offs = torch.zeros(n_rows + 1, dtype=torch.int64, device=rows.device)
+    torch.cumsum(counts, 0, out=offs[1:])
+    return offs
 
 
 def from_host(S, device: int = 0) -> DeviceCSR:

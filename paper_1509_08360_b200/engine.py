@@ -297,7 +297,7 @@ class Plan:
             if block.shape != (n, self.d):
                 raise ValueError("projection block must be 2-d with one row per vertex")
         if out is None:
-            out = np.empty((n, self.d), dtype=np.float64)
+            out = _lib.host_empty((n, self.d), np.float64)
         n_chunks = (d_global + COLUMN_CHUNK - 1) // COLUMN_CHUNK
         peaks = np.zeros(max(n_stages * order * n_chunks, 1), dtype=np.uint64)
         bad_r, bad_stage = C.c_int(0), C.c_int(0)
@@ -392,6 +392,15 @@ class Plan:
 
 
 _device_cache: dict[tuple, tuple] = {}
+
+
+def release_device_copy(S) -> None:
+    """Drop the cached device copies of S (every dtype / device): the next
+    call that needs S on a device uploads it again."""
+    for key in [k for k in _device_cache if k[0] == id(S)]:
+        ref, dm = _device_cache.pop(key)
+        if ref() is S:
+            dm.close()
 
 
 def device_matrix(S, dtype="float64", device: int = 0) -> DeviceMatrix:
@@ -697,8 +706,20 @@ def install(csemb_module):
             saved.append((mod, name, getattr(mod, name)))
             setattr(mod, name, fn)
 
+    # the reference's callers catch its own exception classes (errors.py:12-17):
+    # re-raise device divergence as csemb.errors.DivergenceError
+    try:
+        ref_divergence = importlib.import_module(f"{csemb_module.__name__}.errors").DivergenceError
+    except (ImportError, AttributeError):
+        ref_divergence = DivergenceError
+
     def seam(S, expansion, block, *, stage=0, n_workers=1, counter=None):
-        return apply_expansion(S, expansion, block, stage=stage, counter=counter)
+        try:
+            return apply_expansion(S, expansion, block, stage=stage, counter=counter)
+        except DivergenceError as exc:
+            if ref_divergence is DivergenceError:
+                raise
+            raise ref_divergence(str(exc)) from exc
 
     def norm(S, cfg):
         return estimate_spectral_norm(S, cfg)

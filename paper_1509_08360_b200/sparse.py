@@ -16,11 +16,22 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _lib
+
 
 def _frozen(a, dtype) -> np.ndarray:
-    out = np.ascontiguousarray(a, dtype=dtype)
-    if out is a:
-        out = out.copy()
+    """A private read-only copy of `a` in `dtype` (the reference's immutable
+    SparseMatrix arrays, sparse.py:20-25).  Large arrays are copied into
+    pinned host memory, so the device upload (csemb_matrix_upload) is a
+    direct DMA instead of a staged pageable copy."""
+    src = np.asarray(a)
+    if src.ndim == 1 and src.nbytes >= (1 << 20):
+        out = _lib.host_empty(src.shape, dtype)
+        np.copyto(out, src, casting="unsafe")
+    else:
+        out = np.ascontiguousarray(src, dtype=dtype)
+        if out is src or out.base is src or np.shares_memory(out, src):
+            out = out.copy()
     out.setflags(write=False)
     return out
 

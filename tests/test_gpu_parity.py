@@ -408,8 +408,46 @@ class TestDeviceBuild:
             D = db.normalized_adjacency(torch.as_tensor(zb[f"adj{i}_edges"], device="cuda"), n).to_host()
             assert np.array_equal(D.values, zb[f"adj{i}_values"]) and np.array_equal(D.col_indices, zb[f"adj{i}_col_indices"])
 
+    def test_normalized_adjacency_edge_cases(self):
+        # the library kernels (csrc/build.cu) against the host builder: host and
+        # device edge arrays, duplicates in both orientations, self-loops,
+        # isolated vertices, an empty / loops-only edge list, larger random
+        # graphs (multi-pass radix sort), the fp32 copy, and range errors
+        import torch
+
+        from paper_1509_08360_b200 import device_build as db
+
+        cases = [(np.array([[0, 1], [1, 0], [1, 1], [2, 3], [3, 2], [2, 3]]), 6),
+                 (np.zeros((0, 2), dtype=np.int64), 5),
+                 (np.array([[4, 4], [0, 0]]), 5)]
+        rng = np.random.default_rng(7)
+        for n in (1, 2, 1000, 65_537, 300_000):
+            cases.append((rng.integers(0, n, size=(4 * n + 3, 2)), n))
+        for edges, n in cases:
+            H = pb.normalized_adjacency(edges, n)
+            for src in (edges, torch.as_tensor(edges, device="cuda")):
+                D = db.normalized_adjacency(src, n)
+                assert D.nnz == H.nnz
+                assert np.array_equal(D.row_offsets.cpu().numpy(), H.row_offsets)
+                assert np.array_equal(D.col_indices.cpu().numpy().astype(np.int64), H.col_indices)
+                assert np.array_equal(D.values.cpu().numpy(), H.values)
+            m32 = D.to_device_matrix("float32")
+            assert np.array_equal(m32.download_values(), H.values.astype(np.float32).astype(np.float64))
+            m32.close()
+        with pytest.raises(ValueError):
+            db.normalized_adjacency(np.array([[0, 5]]), 5)
+        with pytest.raises(ValueError):
+            db.normalized_adjacency(torch.as_tensor([[-1, 2]], device="cuda"), 5)
+
     def test_dilate_matches_host(self):
         from paper_1509_08360_b200 import device_build as db
+
+        for m, n, seed in ((1, 1, 0), (7, 3, 1), (3000, 500, 2)):
+            A = graphs.bag_of_words(m, n, seed=seed, mean_len=5)
+            D = db.dilate(db.from_host(A)).to_host()
+            H = pb.dilate(A)
+            assert np.array_equal(D.row_offsets, H.row_offsets) and np.array_equal(D.col_indices, H.col_indices)
+            assert np.array_equal(D.values, H.values)
 
         A = graphs.bag_of_words(400, 300, seed=3, mean_len=20)
         D = db.dilate(db.from_host(A)).to_host()
