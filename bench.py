@@ -186,7 +186,7 @@ def gather_roof(nnz: int, ld: int, dtype: str, k1_ms: float):
     return roof
 
 
-def live_ceilings(ctx, row_bytes: int):
+def live_ceilings(ctx, row_bytes: int, q_bytes: int = 0):
     """L2 -> SM and HBM ceilings measured now, on this device, next to the
     timed region (same clocks and power state): csemb_diag_bandwidth probes
     (csrc/diag.cu).  Returns GB/s for the streaming / K1-shaped gather / copy
@@ -196,8 +196,10 @@ def live_ceilings(ctx, row_bytes: int):
     from paper_1509_08360_b200 import _lib
 
     out = {}
-    for name, kind, nbytes, reps in (("l2_stream", 0, 48 << 20, 20), ("l2_gather", 1, 48 << 20, 500),
-                                     ("hbm_copy", 2, 1 << 30, 1)):
+    probes = [("l2_stream", 0, 48 << 20, 20), ("l2_gather", 1, 48 << 20, 500), ("hbm_copy", 2, 1 << 30, 1)]
+    if q_bytes > (48 << 20):  # the same gather over a window the size of Q(r-1) (DRAM misses included)
+        probes.append(("gather_q_window", 1, q_bytes, 500))
+    for name, kind, nbytes, reps in probes:
         v = C.c_double(0.0)
         _lib.check(ctx.lib.csemb_diag_bandwidth(ctx.handle, kind, nbytes, row_bytes, reps, C.byref(v)),
                    "csemb_diag_bandwidth")
@@ -216,10 +218,11 @@ def fabric_roof(ctx, nnz: int, n: int, d: int, ld: int, dtype: str, k1_ms: float
     streams = nnz * (4 + es) + n * ld * es * (1 + 2.0 / 3.0)
     total = gathered + streams
     ach = total / (k1_ms * 1e-3) / 1e9
-    live = live_ceilings(ctx, min(768, ld * es))
+    live = live_ceilings(ctx, min(768, ld * es), n * ld * es)
     return {"bytes_per_launch": int(total), "gathered_bytes_per_launch": gathered, "achieved": round(ach, 1),
             "unit": "GB/s", "live_ceilings_gbs": live,
             "frac_of_live_gather": round(ach / live["l2_gather"], 4),
+            "frac_of_live_gather_q_window": round(ach / live["gather_q_window"], 4) if "gather_q_window" in live else None,
             "frac_of_live_stream": round(ach / live["l2_stream"], 4),
             "hbm_frac_of_live_copy": None,  # filled by the caller (algorithmic HBM bytes)
             "source": "csemb_diag_bandwidth (csrc/diag.cu), measured right after the timed region"}

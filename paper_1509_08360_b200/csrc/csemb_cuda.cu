@@ -195,21 +195,29 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
 // lane spill at the 64-register cap that gives 4 CTAs / 32 warps per SM)
 template <typename T, int G, int MODE, int PEAK>
 static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, int sm) {
-    if (vpl == 1) return run_step<T, G, 1, MODE, PEAK>(P, s, sm);
+    // reachable shapes only (choose_group: G >= 2 once a row has 2+ vectors,
+    // so one vector per lane happens for G = 1 and G = 2 only)
+    if constexpr (G == 1) {
+        return vpl == 1 ? run_step<T, 1, 1, MODE, PEAK>(P, s, sm) : cudaErrorInvalidValue;
+    } else {
+        if constexpr (G == 2) {
+            if (vpl == 1) return run_step<T, G, 1, MODE, PEAK>(P, s, sm);
+        }
 #if K1_WIDE_VPL
-    if constexpr (G == 4 || G == 8) {  // experiment: 4-5 vectors per lane (wider lane tiles, fewer rows per warp)
-        if (vpl == 4) return run_step<T, G, 4, MODE, PEAK>(P, s, sm);
-        if (vpl == 5) return run_step<T, G, 5, MODE, PEAK>(P, s, sm);
-    }
+        if constexpr (G == 4 || G == 8) {  // experiment: 4-5 vectors per lane (wider lane tiles, fewer rows per warp)
+            if (vpl == 4) return run_step<T, G, 4, MODE, PEAK>(P, s, sm);
+            if (vpl == 5) return run_step<T, G, 5, MODE, PEAK>(P, s, sm);
+        }
 #endif
-    switch (vpl) {
-        case 2: return run_step<T, G, 2, MODE, PEAK>(P, s, sm);
-        case 3: return run_step<T, G, 3, MODE, PEAK>(P, s, sm);
-        default: return cudaErrorInvalidValue;
+        switch (vpl) {
+            case 2: return run_step<T, G, 2, MODE, PEAK>(P, s, sm);
+            case 3: return run_step<T, G, 3, MODE, PEAK>(P, s, sm);
+            default: return cudaErrorInvalidValue;
+        }
     }
 }
 
-// Target vectors per lane (CSEMB_TARGET_VPL in [1, 3], default 3); the group is
+// Target vectors per lane (CSEMB_TARGET_VPL in [2, 3], default 3); the group is
 // the smallest power of two G with ceil(nv/G) <= target, and one launch covers
 // at most 32*target vectors (wider rows are split into column tiles).
 static int target_vpl() {
@@ -217,9 +225,9 @@ static int target_vpl() {
         const char *e = getenv("CSEMB_TARGET_VPL");
         int v = e ? atoi(e) : 3;
 #if K1_WIDE_VPL
-        return std::min(5, std::max(1, v));
+        return std::min(5, std::max(2, v));
 #else
-        return std::min(3, std::max(1, v));
+        return std::min(3, std::max(2, v));
 #endif
     }();
     return t;
@@ -229,6 +237,11 @@ static int choose_group(int nv) {
     const int tv = target_vpl();
     int g = 1;
     while (g < 32 && (nv + g - 1) / g > tv) g *= 2;
+    // one lane per row loads 16 bytes of 32 different rows per instruction (32
+    // L1 wavefronts): at least 2 lanes per row when the row has 2+ vectors.
+    // Measured (round 2, column-shard widths): f32 d=10 0.309 -> 0.246 ms per
+    // step; unchanged for f64 d=10 (already 2 lanes) and every wider row.
+    if (g == 1 && nv > 1) g = 2;
 #if K1_WIDE_VPL
     if (tv > 3 && g != 4 && g != 8) {  // wide lane tiles exist for 4- and 8-lane groups only
         g = 1;
