@@ -53,6 +53,7 @@ UNIT = "nnz*d*L/s"
 WORKLOAD = ("config2: SBM n=1e6, 100 blocks, deg 15 intra + 5 inter, d=80, L=180, f=1{x>=0.95}, "
             "Omega = sample_projection(n, d, 7), row-normalised")
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+L2_NOTE = "working set >> 126 MB L2 (no flush needed)"
 
 
 def log(*a):
@@ -219,7 +220,21 @@ def fabric_roof(ctx, nnz: int, n: int, d: int, ld: int, dtype: str, k1_ms: float
     total = gathered + streams
     ach = total / (k1_ms * 1e-3) / 1e9
     live = live_ceilings(ctx, min(768, ld * es), n * ld * es)
+    # K1's gathers hit L2 at the ncu-measured rate (profiles/k1_traffic.json): the
+    # hit share streams at the L2-resident gather ceiling, the miss share at the
+    # ceiling of the same gathers spread over a Q(r-1)-sized window
+    model = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            hit = json.load(fh)["l2_hit_rate"][dtype]
+        if "gather_q_window" in live:
+            model = {"l2_hit_rate": hit, "model_gbs": round(1.0 / (hit / live["l2_gather"] +
+                                                                   (1 - hit) / live["gather_q_window"]), 1)}
+            model["frac_of_model"] = round(ach / model["model_gbs"], 4)
+    except (OSError, KeyError, ValueError):
+        pass
     return {"bytes_per_launch": int(total), "gathered_bytes_per_launch": gathered, "achieved": round(ach, 1),
+            "live_gather_model": model,
             "unit": "GB/s", "live_ceilings_gbs": live,
             "frac_of_live_gather": round(ach / live["l2_gather"], 4),
             "frac_of_live_gather_q_window": round(ach / live["gather_q_window"], 4) if "gather_q_window" in live else None,
@@ -386,8 +401,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "data": "synthetic (seeded O(T) SBM sampler; the reference's SplitMix64 projection, on device)",
             "config": {"workload": WORKLOAD,
                        "n": n, "nnz": nnz, "d": d, "L": L,
-                       "parallelism": f"column-shard x{world}" if world > 1 else "1 GPU",
-                       "l2": "working set >> 126 MB L2 (no flush needed)"},
+                       "parallelism": f"column-shard x{world}" if world > 1 else "none (one device)",
+                       "l2": L2_NOTE},
             "roofline": res64["roofline"], "clocks": res64["clocks"],
             "gpu_launches": res64["gpu_launches_per_step"] * args.steps,
             "e2e": None if e2e is None else {k: e2e[k] for k in ("value", "unit", "h2d_bytes_per_step",
@@ -808,7 +823,7 @@ def run_reference(args, rank: int, world: int):
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded O(T) SBM sampler; the reference's SplitMix64 projection)",
         "config": {"workload": WORKLOAD, "n": S.n_rows, "nnz": S.nnz, "d": d, "L": L,
-                   "parallelism": f"CPU threads x{cores}"},
+                   "parallelism": "none (one device)", "l2": L2_NOTE},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
