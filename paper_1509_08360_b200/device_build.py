@@ -79,13 +79,15 @@ class DeviceCSR:
             _lib.check(self.owner.lib.csemb_matrix_convert(self.owner.handle, dtype_code(dtype), C.byref(h)),
                        "csemb_matrix_convert")
             return DeviceMatrix(None, dtype, dev, _handle=h)
-        ci = self.col_indices
+        ro, ci, va = self.row_offsets, self.col_indices, self.values
+        if va.device.index != dev:  # the library's kernels read device-local arrays only
+            ro, ci, va = (t.to(f"cuda:{dev}") for t in (ro, ci, va))
         # the tensors may still be in flight on torch's stream (NCCL broadcasts of
-        # distributed.broadcast_matrix, builder kernels): the library stream must
-        # not read them before that work completes
-        torch.cuda.current_stream(self.values.device).synchronize()
-        return DeviceMatrix.from_device(self.n_rows, self.n_cols, self.nnz, self.row_offsets.data_ptr(),
-                                        ci.data_ptr(), ci.element_size(), self.values.data_ptr(), dtype, dev)
+        # distributed.broadcast_matrix, builder kernels, the copy above): the
+        # library stream must not read them before that work completes
+        torch.cuda.current_stream(va.device).synchronize()
+        return DeviceMatrix.from_device(self.n_rows, self.n_cols, self.nnz, ro.data_ptr(),
+                                        ci.data_ptr(), ci.element_size(), va.data_ptr(), dtype, dev)
 
     def to_host(self):
         from .sparse import SparseMatrix

@@ -605,6 +605,56 @@ class TestRowPartition:
         for p in range(1, world):
             assert torch.equal(F[p][L & 1][:n], F[0][L & 1][:n])
 
+    @pytest.mark.parametrize("dtype", ["float64", "float32"])
+    def test_fused_peer_exchange_emulated_power_law(self, dtype):
+        # the fused exchange at scale on a power-law graph: Chung-Lu n = 1e6
+        # (device-built), 3 emulated ranks, rows above the split threshold
+        # chunked on every rank exactly as on one GPU -- the heavy-row combine
+        # kernel stores its Q(r) rows into the peers' replicas too.  Bit-identical
+        # to the single-GPU run with the same (default) schedule.
+        import torch
+
+        from paper_1509_08360_b200 import device_build as db
+        from paper_1509_08360_b200.distributed import row_blocks
+
+        n, d, L, world = 1_000_000, 40, 6, 3
+        S = db.normalized_adjacency(db.chung_lu_edges(n, seed=11), n)
+        assert int((S.row_offsets[1:] - S.row_offsets[:-1]).max()) > 2048  # split rows present
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), L).coeffs
+        dm1 = S.to_device_matrix(dtype)
+        ref = dm1.plan(d).apply(th, 1, None, omega_kind=1, seed=3)
+        dm1.close()
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        n_pad, blocks = row_blocks(n, world)
+        F = [[torch.zeros((world * n_pad, d), dtype=tdt, device="cuda") for _ in range(2)] for _ in range(world)]
+        torch.cuda.synchronize()
+        ro, ci, va = S.row_offsets, S.col_indices, S.values
+        ranks = []
+        for p, (lo, hi) in enumerate(blocks):
+            a, b = int(ro[lo]), int(ro[hi])
+            part = db.DeviceCSR(hi - lo, n, (ro[lo:hi + 1] - a).contiguous(), ci[a:b].contiguous(),
+                                va[a:b].contiguous())
+            dm = part.to_device_matrix(dtype)
+            plan = dm.plan(d)
+            others = [q for q in range(world) if q != p]
+            plan.partition_peers(lo, n, (F[p][0].data_ptr(), F[p][1].data_ptr()),
+                                 [F[q][0].data_ptr() for q in others], [F[q][1].data_ptr() for q in others])
+            plan.begin(th, omega_kind=1, seed=3)
+            ranks.append((dm, plan))
+        for dm, _ in ranks:
+            dm.ctx.sync()
+        for r in range(1, L + 1):
+            for _, plan in ranks:  # independent launches: no rank waits on another
+                plan.step(r)
+            for dm, _ in ranks:  # the per-step barrier
+                dm.ctx.sync()
+        got = []
+        for dm, plan in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        assert np.array_equal(np.concatenate(got), ref)
+
     def test_fused_peer_exchange_errors(self):
         S = graphs.sbm(500, 2, 6.0, 2.0, seed=1)
         dm = pb.DeviceMatrix(S)
