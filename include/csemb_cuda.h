@@ -97,8 +97,8 @@ int csemb_matrix_device_arrays(csemb_mat *m, void **row_offsets, void **col_indi
  *   CSEMB_DIAG_L2_STREAM  coalesced 16-byte .cg re-reads of an L2-resident
  *                         `bytes` buffer, `reps` passes (L2 -> SM fabric)
  *   CSEMB_DIAG_L2_GATHER  K1's load shape: random rows of `row_bytes` inside
- *                         an L2-resident `bytes` window, 16 lanes per row,
- *                         4 rows in flight per lane group, 4*reps rows each
+ *                         a `bytes` window, K1's lanes per row (16 for 640 B,
+ *                         8 for 320 B), 4 rows in flight per lane group
  *   CSEMB_DIAG_HBM_COPY   read + write of a `bytes` buffer (DRAM copy)   */
 #define CSEMB_DIAG_L2_STREAM 0
 #define CSEMB_DIAG_L2_GATHER 1

@@ -8,9 +8,10 @@
 // (same clocks / power state), the ceilings of the second:
 //   CSEMB_DIAG_L2_STREAM : coalesced 16-byte .cg loads re-reading an
 //                          L2-resident buffer (the fabric's streaming rate)
-//   CSEMB_DIAG_L2_GATHER : K1's load shape -- 16 lanes x 3 x 16 B per
-//                          640-byte row (or row_bytes), rows at random inside
-//                          an L2-resident window, 4 rows in flight per lane
+//   CSEMB_DIAG_L2_GATHER : K1's load shape -- G lanes x up to 3 x 16 B per
+//                          row of row_bytes (G as K1 picks it: 16 for
+//                          640-byte rows, 8 for 320-byte rows), rows at random
+//                          inside the window, 4 rows in flight per lane group
 //   CSEMB_DIAG_HBM_COPY  : read + write of a DRAM-sized buffer (the
 //                          MEASURED_PEAKS definition, at these clocks)
 // They are measurement tools, not part of the embedding path.
@@ -40,12 +41,15 @@ __global__ void k_diag_stream(const float4 *__restrict__ a, int64_t n, int reps,
     if (acc == 1234.5f) *sink = acc;
 }
 
-// 16-lane groups; each lane reads vectors gl, gl+16, gl+32 (< vpr) of a row;
-// 4 rows in flight per group (K1's fp64 d=80 shape: 40 vectors per row)
+// G-lane groups (K1's group for this row width: the smallest power of two
+// with ceil(vpr / G) <= 3); each lane reads vectors gl, gl+G, gl+2G (< vpr) of
+// a row; 4 rows in flight per group (K1's shape: 16 lanes for 640-byte fp64
+// rows, 8 lanes for 320-byte fp32 rows)
+template <int G>
 __global__ void k_diag_gather(const float4 *__restrict__ a, uint32_t nrows, int vpr, uint32_t rows_per_group,
                               float *sink) {
-    const int gl = threadIdx.x & 15;
-    const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+    const int gl = threadIdx.x & (G - 1);
+    const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) / G;
     uint32_t h = g * 2654435761u + 12345u;
     float acc = 0.f;
     for (uint32_t it = 0; it < rows_per_group; it += 4) {
@@ -57,7 +61,7 @@ __global__ void k_diag_gather(const float4 *__restrict__ a, uint32_t nrows, int 
             const float4 *p = a + (size_t)row * vpr + gl;
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                v[u][k] = (gl + 16 * k < vpr) ? __ldg(p + 16 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[u][k] = (gl + G * k < vpr) ? __ldg(p + G * k) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -102,9 +106,17 @@ extern "C" int csemb_diag_bandwidth(csemb_ctx *c, int kind, int64_t bytes, int64
         } else if (kind == CSEMB_DIAG_L2_GATHER) {
             const int vpr = (int)(row_bytes / 16);
             const uint32_t nrows = (uint32_t)(bytes / row_bytes);
-            const uint32_t groups = (uint32_t)sms * 2 * 256 / 16;  // 2 CTAs x 256 threads per SM, as K1
-            const uint32_t per = (uint32_t)std::max<int64_t>(4, (int64_t)reps * 4);
-            k_diag_gather<<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink);
+            int G = 1;
+            while (G < 16 && (vpr + G - 1) / G > 3) G *= 2;
+            const uint32_t groups = (uint32_t)sms * 2 * 256 / G;  // 2 CTAs x 256 threads per SM, as K1
+            const uint32_t per = (uint32_t)std::max<int64_t>(4, (int64_t)reps * 4 * G / 16);
+            switch (G) {
+                case 1: k_diag_gather<1><<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink); break;
+                case 2: k_diag_gather<2><<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink); break;
+                case 4: k_diag_gather<4><<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink); break;
+                case 8: k_diag_gather<8><<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink); break;
+                default: k_diag_gather<16><<<sms * 2, 256, 0, s>>>((const float4 *)a, nrows, vpr, per, (float *)sink);
+            }
             moved = (double)groups * per * row_bytes;
         } else {
             k_diag_copy<<<sms * 8, 512, 0, s>>>((const float4 *)a, (float4 *)b, nvec);
