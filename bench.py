@@ -208,6 +208,30 @@ def live_ceilings(ctx, row_bytes: int, q_bytes: int = 0):
     return out
 
 
+def gather_floor(dm, row_bytes: int, k1_ms: float):
+    """The same-data floor of K1, measured live next to the timed region:
+    csemb_diag_gather_csr fetches, for every stored entry of THIS matrix in
+    stored order, the whole row_bytes-wide row of a Q(r-1)-sized block -- K1's
+    gathered bytes and address stream -- with no arithmetic, no epilogue and
+    no streamed blocks, 4 or 8 entries in flight per lane group (best of the
+    two).  k1_over_floor = how much longer the fused step takes than fetching
+    its gathered rows alone."""
+    import ctypes as C
+
+    from paper_1509_08360_b200 import _lib
+
+    best = None
+    for depth in (4, 8):
+        ms, gbs = C.c_double(0.0), C.c_double(0.0)
+        _lib.check(dm.lib.csemb_diag_gather_csr(dm.handle, row_bytes, depth, C.byref(ms), C.byref(gbs)),
+                   "csemb_diag_gather_csr")
+        if best is None or ms.value < best["ms"]:
+            best = {"ms": round(ms.value, 4), "gathered_gbs": round(gbs.value, 1), "in_flight": depth}
+    best["k1_over_floor"] = round(k1_ms / best["ms"], 3)
+    best["source"] = "csemb_diag_gather_csr (csrc/diag.cu): gather-only pass over the bench matrix, same clocks"
+    return best
+
+
 def fabric_roof(ctx, nnz: int, n: int, d: int, ld: int, dtype: str, k1_ms: float, L: int):
     """K1's L2 -> SM side (the resource a gather SpMM saturates first): bytes
     that cross the fabric per launch -- every stored entry gathers one
@@ -350,6 +374,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         roof["gather"] = gather_roof(nnz, (hi - lo + W - 1) // W * W, dtype, k1_ms)
         roof["l2_fabric"] = fabric_roof(dm.ctx, nnz, n, hi - lo, (hi - lo + W - 1) // W * W, dtype, k1_ms, L)
         roof["l2_fabric"]["hbm_frac_of_live_copy"] = round(achieved / roof["l2_fabric"]["live_ceilings_gbs"]["hbm_copy"], 4)
+        roof["gather_floor"] = gather_floor(dm, (hi - lo + W - 1) // W * W * (8 if dtype == "f64" else 4), k1_ms)
         out = {
             "value": units / (ms * 1e-3), "ms_per_step": ms, "k1_ms": k1_ms,
             "gpu_launches_per_step": launches_per_step,
@@ -652,7 +677,8 @@ def run_configs34(args, peak, peak_src):
                     "k1_launches_per_step": launches / L,
                     "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                                  "frac": round(ach / peak, 4), "algorithmic_bytes_per_launch": B,
-                                 "peak_source": peak_src, "traffic": None}})
+                                 "peak_source": peak_src, "traffic": None,
+                                 "gather_floor": gather_floor(dm, (d + 3) // 4 * 16, k1)}})
         log(f"[bench] config {cfg_id}: embed {tot:.1f} ms (wall {wall_ms:.1f} ms), K1 {k1:.3f} ms/step, "
             f"{ach:.0f} GB/s ({ach / peak:.3f})")
         dm.close()

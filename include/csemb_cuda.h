@@ -104,6 +104,12 @@ int csemb_matrix_device_arrays(csemb_mat *m, void **row_offsets, void **col_indi
 #define CSEMB_DIAG_L2_GATHER 1
 #define CSEMB_DIAG_HBM_COPY 2
 int csemb_diag_bandwidth(csemb_ctx *ctx, int kind, int64_t bytes, int64_t row_bytes, int reps, double *gbs);
+/* Gather-only pass over m: every stored entry fetches one `row_bytes` row of
+ * an n_cols-row block (K1's gathered bytes, in stored order, K1's lanes per
+ * row), no arithmetic or streamed blocks, `in_flight` (4 | 8) entries in
+ * flight per lane group.  Best of 3 timed launches: ms per pass and the
+ * gathered GB/s (nnz * row_bytes / time).  The floor for K1 on m. */
+int csemb_diag_gather_csr(csemb_mat *m, int64_t row_bytes, int in_flight, double *ms, double *gbs);
 
 /* ---- device-side input construction --------------------
  * normalized_adjacency (sparse.py:202-226): edges is an n_edges x 2 int64

@@ -60,6 +60,7 @@ SIGNATURES = {
     "csemb_build_normalized_adjacency": (_int, [_p, _i64, _i64, _p, _int, _int, _pp]),
     "csemb_build_dilation": (_int, [_p, _pp]),
     "csemb_diag_bandwidth": (_int, [_p, _int, _i64, _i64, _int, _pd]),
+    "csemb_diag_gather_csr": (_int, [_p, _i64, _int, _pd, _pd]),
     "csemb_plan_create": (_int, [_p, _i64, _pp]),
     "csemb_plan_destroy": (_int, [_p]),
     "csemb_plan_set_option": (_int, [_p, _int, _i64]),

@@ -33,3 +33,13 @@ for _ in range(args.reps):
     tot, steps, launches = plan.timing()
     print(f"{args.dtype}: L={args.L} total {tot:.3f} ms, K1 avg {steps / max(launches, 1):.3f} ms "
           f"({launches} launches), wall {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
+
+if os.environ.get("CSEMB_PROFILE_FLOOR"):  # the same-data gather floor (csemb_diag_gather_csr), for ncu
+    import ctypes as C
+
+    es = 8 if args.dtype == "f64" else 4
+    W = 16 // es
+    ms, gbs = C.c_double(), C.c_double()
+    _lib.check(dm.lib.csemb_diag_gather_csr(dm.handle, (args.d + W - 1) // W * W * es, 4, C.byref(ms), C.byref(gbs)),
+               "floor")
+    print(f"gather floor {ms.value:.4f} ms ({gbs.value:.0f} GB/s)")
