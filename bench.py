@@ -200,6 +200,8 @@ def live_ceilings(ctx, row_bytes: int, q_bytes: int = 0):
     probes = [("l2_stream", 0, 48 << 20, 20), ("l2_gather", 1, 48 << 20, 500), ("hbm_copy", 2, 1 << 30, 1)]
     if q_bytes > (48 << 20):  # the same gather over a window the size of Q(r-1) (DRAM misses included)
         probes.append(("gather_q_window", 1, q_bytes, 500))
+    # ... and over a 4 GiB window (>97% L2 misses): the HBM ceiling for random row reads of this width
+    probes.append(("gather_dram", 1, 4 << 30, 500))
     for name, kind, nbytes, reps in probes:
         v = C.c_double(0.0)
         _lib.check(ctx.lib.csemb_diag_bandwidth(ctx.handle, kind, nbytes, row_bytes, reps, C.byref(v)),
@@ -375,6 +377,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         roof["l2_fabric"] = fabric_roof(dm.ctx, nnz, n, hi - lo, (hi - lo + W - 1) // W * W, dtype, k1_ms, L)
         roof["l2_fabric"]["hbm_frac_of_live_copy"] = round(achieved / roof["l2_fabric"]["live_ceilings_gbs"]["hbm_copy"], 4)
         roof["gather_floor"] = gather_floor(dm, (hi - lo + W - 1) // W * W * (8 if dtype == "f64" else 4), k1_ms)
+        if traffic:
+            # K1 against HBM on its ACTUAL traffic (ncu bytes per launch over the live K1
+            # time): between the live random-row ceiling (its gathers' misses) and the
+            # live copy ceiling (its streams)
+            live = roof["l2_fabric"]["live_ceilings_gbs"]
+            dram_gbs = traffic / (k1_ms * 1e-3) / 1e9
+            roof["dram"].update({"live_random_row_gbs": live.get("gather_dram"), "live_copy_gbs": live["hbm_copy"],
+                                 "frac_of_live_random_row": round(dram_gbs / live["gather_dram"], 4)
+                                 if live.get("gather_dram") else None,
+                                 "frac_of_live_copy": round(dram_gbs / live["hbm_copy"], 4)})
         out = {
             "value": units / (ms * 1e-3), "ms_per_step": ms, "k1_ms": k1_ms,
             "gpu_launches_per_step": launches_per_step,

@@ -84,6 +84,11 @@ int csemb_matrix_info(csemb_mat *m, int64_t *n_rows, int64_t *n_cols, int64_t *n
 /* scale_values (sparse.py:295-301): values *= factor on the device (same
  * IEEE product as numpy's S.values * factor). */
 int csemb_matrix_scale(csemb_mat *m, double factor);
+/* 1 if every stored value of m is bit-identical to normalized_adjacency's
+ * 1/sqrt(deg(u) deg(v)) with deg = the stored row lengths (sparse.py:224):
+ * K1 then recomputes values instead of streaming them (CSEMB_OPT_VALUE_FREE).
+ * Runs the device check on first use; csemb_matrix_scale clears it. */
+int csemb_matrix_value_free(csemb_mat *m, int *out);
 /* copy the device values back (f64) -- for tests of csemb_matrix_scale */
 int csemb_matrix_download_values(csemb_mat *m, double *values_out);
 /* a copy of m in another arithmetic type (values converted; CSR shared shape) */
@@ -156,6 +161,15 @@ int csemb_plan_destroy(csemb_plan *p);
                                        csemb_plan_run with an identical signature
                                        (coefficients, options, block pointer, seed, slice)
                                        is captured as a CUDA graph, later ones replay it */
+#define CSEMB_OPT_VALUE_FREE 7      /* -1 default (off unless CSEMB_VALUE_FREE=1), 0 off, 1 on:
+                                       when every stored value of the matrix is bit-identical to
+                                       normalized_adjacency's 1/sqrt(deg(u) deg(v)) with deg = the
+                                       stored row lengths (sparse.py:224; checked once on the
+                                       device), K1 recomputes it from the row offsets instead of
+                                       streaming the values (bit-identical results; whole rows
+                                       only -- split heavy-row chunks and row partitions read
+                                       the values).  Measured slower than streaming the values
+                                       (a dependent gather + IEEE sqrt/div per entry), so off */
 #define CSEMB_OPT_E_FOLD 5           /* 1..3 (default 3): E is read and written every
                                        e_fold steps; a flush adds the pending terms in
                                        the reference's order, so results are unchanged */

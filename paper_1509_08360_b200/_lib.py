@@ -22,6 +22,7 @@ OK, ERR_INVALID, ERR_CUDA, ERR_NOMEM, ERR_DIVERGED, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 OMEGA_GIVEN, OMEGA_SPLITMIX, OMEGA_PHILOX = 0, 1, 2
 OPT_EXACT_PEAKS, OPT_REVERSE_SWEEP, OPT_SPLIT_THRESHOLD, OPT_ROW_ORDER, OPT_E_FOLD, OPT_GRAPH = 1, 2, 3, 4, 5, 6
+OPT_VALUE_FREE = 7
 
 DIVERGENCE_MESSAGE = (
     "iteration r={r} produced non-finite values; the matrix likely has "
@@ -54,6 +55,7 @@ SIGNATURES = {
     "csemb_matrix_destroy": (_int, [_p]),
     "csemb_matrix_info": (_int, [_p, _pi64, _pi64, _pi64, _pi]),
     "csemb_matrix_scale": (_int, [_p, _dbl]),
+    "csemb_matrix_value_free": (_int, [_p, _pi]),
     "csemb_matrix_download_values": (_int, [_p, _p]),
     "csemb_matrix_convert": (_int, [_p, _int, _pp]),
     "csemb_matrix_device_arrays": (_int, [_p, _pp, _pp, _pp]),

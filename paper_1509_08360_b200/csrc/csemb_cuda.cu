@@ -60,6 +60,7 @@ struct csemb_plan {
     int64_t split_threshold = DEFAULT_SPLIT;  // 0: never split rows (bit-exact for every input)
     int e_fold = 3;                  // E read/written every e_fold steps (1..3), same roundings
     int row_order = -1;              // -1 auto, 0 natural, 1 bucketed, 2 windowed (auto window), >= 64 window
+    int value_free = -1;             // -1 default (CSEMB_VALUE_FREE, off), 0 off, 1 on
     void *partials = nullptr;        // heavy-row chunk partial sums
     size_t partials_bytes = 0;
     // row partition (csemb_plan_partition): this plan's matrix holds rows
@@ -295,6 +296,7 @@ static cudaError_t launch_step(StepParams P, const Schedule *sc, void *partials,
             C.peaks = nullptr;
             C.n_peer = 0;  // chunk partial sums stay local
             C.mc = nullptr;
+            C.vf = nullptr;  // chunk extents are not whole rows (the value-free form needs the row length)
             e = dispatch_group<T, MODE_SPMM, PEAK_FLAG>(G, vpl, C, s, sm);
             if (e != cudaSuccess) return e;
             ++nl;
@@ -654,9 +656,53 @@ extern "C" int csemb_ctx_sm_count(csemb_ctx *c, int *out) {
 // ---------------------------------------------------------------------------
 // matrices
 // ---------------------------------------------------------------------------
+// The matrix's value-free flag (device int), checked on first use: the check
+// kernel runs on the context stream ahead of the K1 launches that read it.
+static cudaError_t mat_vf_flag(csemb_mat *m, const int **out) {
+    *out = nullptr;
+    if (m->vf_state < 0) {
+        cudaStream_t s = m->ctx->stream;
+        if (!m->vf_flag) {
+            cudaError_t e = dmalloc(m->ctx, &m->vf_flag, sizeof(int));
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = cudaMemsetAsync(m->vf_flag, 0, sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        if (m->nnz > 0 && m->n_rows > 0) {
+            const int one = 1;
+            e = cudaMemcpyAsync(m->vf_flag, &one, sizeof(int), cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // `one` is a stack value
+            if (e != cudaSuccess) return e;
+            const int g = grid_for(m->n_rows * 32, 256, m->ctx->sm_count, 8);
+            if (m->dtype == CSEMB_F64)
+                k_vf_check<double><<<g, 256, 0, s>>>(m->rowptr, m->cols, (const double *)m->vals, m->n_rows, m->vf_flag);
+            else
+                k_vf_check<float><<<g, 256, 0, s>>>(m->rowptr, m->cols, (const float *)m->vals, m->n_rows, m->vf_flag);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+        m->vf_state = 1;
+    }
+    *out = m->vf_flag;
+    return cudaSuccess;
+}
+
+// Off by default: measured on config-2-sized graphs (profiles/r2_k1_experiments.txt,
+// "value-free"), recomputing the value (a dependent row-offset gather plus
+// an IEEE sqrt and divide per entry) costs far more than streaming it:
+// f64 d=80 1.19 -> 1.51 ms per step, f32 d=10 0.23 -> 0.40 ms.
+static int value_free_default() {
+    static int on = [] {
+        const char *e = getenv("CSEMB_VALUE_FREE");
+        return e ? atoi(e) != 0 : 0;
+    }();
+    return on;
+}
+
 void mat_free(csemb_mat *m) {
     if (!m) return;
     for (Schedule *sc : m->schedules) sched_free(m->ctx, sc);
+    dfree(m->ctx, m->vf_flag);
     dfree(m->ctx, m->rowptr);
     dfree(m->ctx, m->cols);
     dfree(m->ctx, m->vals);
@@ -844,6 +890,19 @@ extern "C" int csemb_matrix_info(csemb_mat *m, int64_t *n_rows, int64_t *n_cols,
     return CSEMB_OK;
 }
 
+extern "C" int csemb_matrix_value_free(csemb_mat *m, int *out) {
+    if (!m || !out) return fail(CSEMB_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    CK(cudaSetDevice(m->ctx->device));
+    const int *flag = nullptr;
+    CK(mat_vf_flag(m, &flag));
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, m->ctx->stream));
+    CK(cudaStreamSynchronize(m->ctx->stream));
+    *out = h;
+    return CSEMB_OK;
+}
+
 extern "C" int csemb_matrix_scale(csemb_mat *m, double factor) {
     if (!m) return fail(CSEMB_ERR_INVALID, "null matrix");
     if (factor == 0.0 || !std::isfinite(factor))
@@ -851,6 +910,8 @@ extern "C" int csemb_matrix_scale(csemb_mat *m, double factor) {
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     CK(cudaSetDevice(m->ctx->device));
     if (m->nnz == 0) return CSEMB_OK;
+    if (m->vf_flag) CK(cudaMemsetAsync(m->vf_flag, 0, sizeof(int), m->ctx->stream));  // no longer the formula
+    m->vf_state = m->vf_flag ? 1 : -1;
     const int g = grid_for(m->nnz, 256, m->ctx->sm_count);
     if (m->dtype == CSEMB_F64)
         k_vals_scale<double><<<g, 256, 0, m->ctx->stream>>>((double *)m->vals, m->nnz, factor);
@@ -935,6 +996,7 @@ extern "C" int csemb_plan_set_option(csemb_plan *p, int option, int64_t value) {
     switch (option) {
         case CSEMB_OPT_EXACT_PEAKS: p->exact_peaks = value != 0; return CSEMB_OK;
         case CSEMB_OPT_REVERSE_SWEEP: p->reverse_sweep = value != 0; return CSEMB_OK;
+        case CSEMB_OPT_VALUE_FREE: p->value_free = value < 0 ? -1 : (value != 0); return CSEMB_OK;
         case CSEMB_OPT_SPLIT_THRESHOLD:
             if (value < 0) return fail(CSEMB_ERR_INVALID, "split threshold must be >= 0");
             p->split_threshold = value;
@@ -1025,6 +1087,8 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
             p->partials_bytes = pbytes;
         }
     }
+    const int *vf = nullptr;
+    if (p->value_free > 0 || (p->value_free < 0 && value_free_default())) CK(mat_vf_flag(m, &vf));
     CK(rec_event(p, 0, s));
     for (int st = 0; st < n_stages; ++st) {
         const int kind = st > 0 ? OMEGA_FROM_E : omega_kind;
@@ -1056,6 +1120,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
             P.reverse = p->reverse_sweep && (r & 1) == 0;
             P.peaks = p->peaks + ((size_t)st * order + (r - 1)) * n_chunks;
             P.col0 = (int)col0;
+            P.vf = vf;
             if (n > 0) {
                 if (p->exact_peaks)
                     CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, sc, p->partials, s, c->sm_count, &p->step_launches));
@@ -1115,7 +1180,8 @@ static int plan_run_locked(csemb_plan *p, const double *coeffs, int order, int n
         sig.insert(sig.end(), (const unsigned char *)v, (const unsigned char *)v + nb);
     };
     const int64_t ints[] = {order, n_stages, omega_kind, col0, d_global, normalize_rows, p->exact_peaks,
-                            p->e_fold, p->reverse_sweep, p->split_threshold, p->row_order, p->m->dtype};
+                            p->e_fold, p->reverse_sweep, p->split_threshold, p->row_order, p->m->dtype,
+                            p->value_free};
     put(ints, sizeof ints);
     put(&seed, sizeof seed);
     put(&block_dev, sizeof block_dev);

@@ -168,7 +168,26 @@ struct StepParams {
     // ranks' replicas, this one included): one multimem store per 8 bytes that
     // the NVSwitch replicates, instead of n_peer unicast stores
     void *mc;
+    // value-free normalized adjacency (csemb_plan option CSEMB_OPT_VALUE_FREE):
+    // when *vf != 0 every stored value equals 1/sqrt(len(row) * len(col)) with
+    // len = the stored row lengths (sparse.normalized_adjacency, sparse.py:224,
+    // checked bit for bit on the device by k_vf_check), so K1 recomputes the
+    // value from the row offsets instead of streaming it (null: read values)
+    const int *vf;
 };
+
+__device__ __forceinline__ bool memcmp_eq(double a, double b) { return __double_as_longlong(a) == __double_as_longlong(b); }
+__device__ __forceinline__ bool memcmp_eq(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+
+// the reference's normalized-adjacency value, 1.0 / np.sqrt(deg[u] * deg[v])
+// (sparse.py:224): exact integer product (< 2^53), IEEE sqrt and division,
+// each correctly rounded -- then the run dtype's conversion, as the stored
+// value got it
+template <typename T>
+__device__ __forceinline__ T vf_value(double len_row, const int64_t *__restrict__ rowptr, int j) {
+    const int64_t lj = __ldg(rowptr + j + 1) - __ldg(rowptr + j);
+    return (T)__ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(len_row, (double)lj)));
+}
 
 // bit-exact 16-byte store through a multicast address (two multimem.st.b64;
 // the vector forms take float types only)
@@ -354,6 +373,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     const T theta1 = (T)P.theta1, theta2 = (T)P.theta2;
     const bool has_prev = P.has_prev != 0;
     const int first_chunk = (P.col0 + P.v0 * W) >> 5;
+    const bool vfree = P.vf != nullptr && *P.vf != 0;  // warp-uniform
 
     bool valid[VPL];
 #pragma unroll
@@ -396,7 +416,8 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     constexpr int B = EB > 1 ? G * EB : ((K1_BATCH > 0 && K1_BATCH < G) ? K1_BATCH : G);
     static_assert(EB > 1 || G % B == 0, "batch width must divide the group width");
     constexpr int BL = EB > 1 ? G : B;  // lanes that hold the batch
-    auto load_batch = [&](int64_t b0, int64_t e0, int (&j)[EB], T (&a)[EB]) {
+    // len: the row's stored length (its degree, for the value-free form)
+    auto load_batch = [&](int64_t b0, int64_t e0, int64_t len, int (&j)[EB], T (&a)[EB]) {
 #pragma unroll
         for (int k = 0; k < EB; ++k) {
             j[k] = 0;
@@ -404,7 +425,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             const int64_t q = b0 + gl + k * G;
             if (gl < BL && q < e0) {
                 j[k] = __ldcs(cols + q);
-                a[k] = __ldcs(vals + q);
+                if (vfree)
+                    a[k] = vf_value<T>((double)len, P.rowptr, j[k]);
+                else
+                    a[k] = __ldcs(vals + q);
             }
         }
     };
@@ -413,7 +437,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     auto bcast_a = [&](const T (&a)[EB], int t) { return __shfl_sync(0xFFFFFFFFu, a[t / G], t % G, G); };
     int myj[EB];
     T mya[EB];
-    load_batch(beg, end, myj, mya);
+    load_batch(beg, end, end - beg, myj, mya);
 
     // Gathers of the first D-1 entries of the current batch are carried across
     // batches.  Register variant: D-deep rotating register buffer.  Staged
@@ -527,10 +551,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             int ncnt = 0;  // entries of that next batch for my row
             if (b + 1 < nb_mine) {
                 ncnt = len - (b + 1) * B;
-                load_batch(beg + (b + 1) * B, end, nj, na);
+                load_batch(beg + (b + 1) * B, end, end - beg, nj, na);
             } else if (b + 1 >= nb) {
                 ncnt = (int)(end2 - beg2);
-                load_batch(beg2, end2, nj, na);
+                load_batch(beg2, end2, end2 - beg2, nj, na);
             } else {
 #pragma unroll
                 for (int k = 0; k < EB; ++k) {
@@ -620,7 +644,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             }
         }
         if (nb == 0) {  // every row of the warp is empty: move to the next rows' first batch
-            load_batch(beg2, end2, myj, mya);
+            load_batch(beg2, end2, end2 - beg2, myj, mya);
 #pragma unroll
             for (int e = 0; e < D - 1; ++e) issue(e, bcast_j(myj, e), e < end2 - beg2);
         }
@@ -869,6 +893,27 @@ __device__ __forceinline__ bool omega_sign(int kind, uint64_t key, uint64_t seed
 }
 
 // Q(0) = block, E = theta0 * block; pad columns [d, ld) are zero.
+// Value-free detection: *ok stays 1 only if every stored value equals
+// vf_value(len(row), len(col)) bit for bit (one warp per row, lanes over its
+// entries); a zero-length column (1/sqrt(0) = inf) never matches a finite value.
+template <typename T>
+__global__ void k_vf_check(const int64_t *__restrict__ rowptr, const int *__restrict__ cols,
+                           const T *__restrict__ vals, int64_t n_rows, int *ok) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w0; r < n_rows; r += nw) {
+        if (*(volatile int *)ok == 0) return;
+        const int64_t b = rowptr[r], e = rowptr[r + 1];
+        bool good = true;
+        for (int64_t q = b + lane; q < e; q += 32) good &= memcmp_eq(vf_value<T>((double)(e - b), rowptr, cols[q]), vals[q]);
+        if (!__all_sync(0xFFFFFFFFu, good)) {
+            if (lane == 0) *ok = 0;
+            return;
+        }
+    }
+}
+
 template <typename T>
 __global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int64_t n, int d,
                              int ld, int kind, uint64_t seed, int64_t col0, int64_t d_global,

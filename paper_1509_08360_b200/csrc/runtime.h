@@ -85,6 +85,11 @@ struct csemb_mat {
     void *vals = nullptr;
     std::vector<int64_t> rowptr_host;
     std::vector<Schedule *> schedules;
+    // value-free normalized adjacency (kernels.cuh k_vf_check / vf_value): a
+    // device int, 1 while every stored value is 1/sqrt(len(row) len(col));
+    // checked once, lazily, on the context stream (-1 = not checked yet)
+    int *vf_flag = nullptr;
+    int vf_state = -1;
 };
 
 CSEMB_INTERNAL size_t dsize(int dtype);

@@ -201,6 +201,15 @@ class DeviceMatrix:
         """values *= factor in place (scale_values, sparse.py:295-301)."""
         _lib.check(self.lib.csemb_matrix_scale(self.handle, float(factor)), "csemb_matrix_scale")
 
+    @property
+    def value_free(self) -> bool:
+        """True when every stored value is normalized_adjacency's
+        1/sqrt(deg u * deg v) bit for bit (sparse.py:224), so K1 recomputes the
+        values from the row offsets instead of streaming them."""
+        v = C.c_int(0)
+        _lib.check(self.lib.csemb_matrix_value_free(self.handle, C.byref(v)), "csemb_matrix_value_free")
+        return bool(v.value)
+
     def spectral_norm(self, iters: int, k: int, seed: int, safety: float = 1.01, v0=None) -> float:
         """Device power iteration (estimate_spectral_norm, engine.py:165-192) on
         this resident matrix; v0=None draws the start block with Philox."""

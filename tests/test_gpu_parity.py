@@ -17,7 +17,7 @@ import pytest
 import oracle as O
 import paper_1509_08360_b200 as pb
 from conftest import csr_from, load_golden, sparse_from
-from paper_1509_08360_b200 import graphs
+from paper_1509_08360_b200 import _lib, graphs
 
 pytestmark = pytest.mark.gpu
 
@@ -809,9 +809,9 @@ class TestEFold:
         ref = _oracle_embed(S, th, om)
         for fold in (1, 2, 3):
             plan = pb.device_matrix(S).plan(24)
-            plan.set_option(pb._lib.OPT_E_FOLD, fold)
+            plan.set_option(_lib.OPT_E_FOLD, fold)
             assert np.array_equal(plan.apply(th, 1, om), ref), (L, fold)
-            plan.set_option(pb._lib.OPT_E_FOLD, 3)
+            plan.set_option(_lib.OPT_E_FOLD, 3)
 
     def test_cascade_stages(self):
         S = graphs.sbm(1200, 4, 8.0, 2.0, seed=9)
@@ -843,7 +843,7 @@ class TestABIErrors:
         with pytest.raises(ValueError, match="begin"):
             plan.step(1)
         with pytest.raises(ValueError):
-            plan.set_option(pb._lib.OPT_E_FOLD, 7)
+            plan.set_option(_lib.OPT_E_FOLD, 7)
         with pytest.raises(ValueError):
             plan.set_option(99, 1)
         with pytest.raises(ValueError):
@@ -947,21 +947,21 @@ def test_graph_replay_bit_exact(config1):
     dm = pb.DeviceMatrix(S, "float64")
     plan = dm.plan(40)
     for mode in (1, 0, -1):
-        plan.set_option(pb._lib.OPT_GRAPH, mode)
+        plan.set_option(_lib.OPT_GRAPH, mode)
         for _ in range(4):
-            plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+            plan.run(z["coeffs"], 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=0)
             assert sha(plan.download()) == meta["E_sha256"]
             tot, steps, launches = plan.timing()
             assert tot > 0 and steps > 0 and launches == 60
     other, _, _ = O.apply_expansion(O.CSR.of(S), z["coeffs"][:31], O.sample_projection(2000, 40, 3))
-    plan.set_option(pb._lib.OPT_GRAPH, 1)
+    plan.set_option(_lib.OPT_GRAPH, 1)
     for _ in range(3):
-        plan.run(z["coeffs"][:31], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=3)
+        plan.run(z["coeffs"][:31], 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=3)
         assert np.array_equal(plan.download(), other)
-        plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+        plan.run(z["coeffs"], 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=0)
         assert sha(plan.download()) == meta["E_sha256"]
     with pytest.raises(ValueError):
-        plan.set_option(pb._lib.OPT_GRAPH, 2)
+        plan.set_option(_lib.OPT_GRAPH, 2)
     dm.close()
 
 
@@ -973,7 +973,7 @@ def test_graph_survives_buffer_reallocation(config1):
     S = sparse_from(z)
     dm = pb.DeviceMatrix(S, "float64")
     plan = dm.plan(40)
-    plan.set_option(pb._lib.OPT_GRAPH, 1)
+    plan.set_option(_lib.OPT_GRAPH, 1)
     plan.set_exact_peaks(True)
     om = O.sample_projection(2000, 40, 0)
     refs = {}
@@ -982,7 +982,7 @@ def test_graph_survives_buffer_reallocation(config1):
         if L not in refs:
             refs[L] = O.run_stage(O.CSR.of(S), th, om)
         ref, ref_peaks, _ = refs[L]
-        plan.run(th, 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+        plan.run(th, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=0)
         assert np.array_equal(plan.download(), ref), L
         peaks, bad, _ = plan.diagnostics()
         assert bad == 0 and peaks.shape == (1, L, 2)
@@ -998,7 +998,7 @@ def test_out_of_memory_is_reported_and_context_survives(config1):
     with pytest.raises(MemoryError):
         dm.plan(1_000_000_000)  # 3 x 2000 x 1e9 doubles
     plan = dm.plan(40)
-    plan.run(z["coeffs"], 1, omega_kind=pb._lib.OMEGA_SPLITMIX, seed=0)
+    plan.run(z["coeffs"], 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=0)
     assert sha(plan.download()) == meta["E_sha256"]
     dm.close()
 
@@ -1013,7 +1013,7 @@ def test_repeated_create_destroy_does_not_grow_memory(config1):
 
     def cycle():
         dm = pb.DeviceMatrix(S, "float64")
-        out = dm.plan(40).apply(z["coeffs"], 1, None, omega_kind=pb._lib.OMEGA_SPLITMIX)
+        out = dm.plan(40).apply(z["coeffs"], 1, None, omega_kind=_lib.OMEGA_SPLITMIX)
         dm.close()
         return out
 
@@ -1114,3 +1114,76 @@ def test_config2_full_scale_fp64_bit_exact_and_fp32_gates():
 
 
 # configs 3 / 4 / 5 at full shape against the oracle: tests/test_gpu_scale.py
+
+
+# --------------------------------------------------------------------------
+# value-free normalized adjacency (CSEMB_OPT_VALUE_FREE): K1 recomputes
+# 1/sqrt(deg u * deg v) (sparse.py:224) from the row offsets
+# --------------------------------------------------------------------------
+class TestValueFree:
+    def test_detected_on_normalized_adjacency_and_bit_exact(self, config1):
+        z, meta = config1
+        S = sparse_from(z)
+        th = pb.legendre_coefficients(pb.indicator_above(0.9), 60).coeffs
+        om = O.sample_projection(2000, 40, 0)
+        for dt in ("float64", "float32"):
+            dm = pb.DeviceMatrix(S, dt)
+            assert dm.value_free
+            plan = dm.plan(40)
+            plan.set_option(_lib.OPT_VALUE_FREE, 1)
+            on = plan.apply(th, 1, om)
+            plan.set_option(_lib.OPT_VALUE_FREE, 0)
+            off = plan.apply(th, 1, om)
+            assert np.array_equal(on, off)
+            if dt == "float64":
+                assert sha(on) == meta["E_sha256"]
+            dm.close()
+
+    def test_not_detected_on_other_values(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        vals = np.asarray(S.values).copy()
+        vals[len(vals) // 2] = np.nextafter(vals[len(vals) // 2], 1.0)  # one ulp off the formula
+        T = pb.SparseMatrix(S.n_rows, S.n_cols, S.row_offsets, S.col_indices, vals)
+        dm = pb.DeviceMatrix(T, "float64")
+        assert not dm.value_free
+        th = pb.legendre_coefficients(pb.indicator_above(0.9), 20).coeffs
+        om = O.sample_projection(2000, 40, 0)
+        plan = dm.plan(40)
+        plan.set_option(_lib.OPT_VALUE_FREE, 1)  # requested, but the check says no: values are read
+        assert np.array_equal(plan.apply(th, 1, om), _oracle_embed(T, th, om))
+        dm.close()
+
+    def test_scale_clears_it(self, config1):
+        z, _ = config1
+        S = sparse_from(z)
+        dm = pb.DeviceMatrix(S, "float64")
+        plan = dm.plan(40)
+        plan.set_option(_lib.OPT_VALUE_FREE, 1)
+        th = pb.legendre_coefficients(pb.indicator_above(0.9), 12).coeffs
+        om = O.sample_projection(2000, 40, 0)
+        plan.apply(th, 1, om)  # the check ran and cached "on"
+        assert dm.value_free
+        dm.scale(0.5)
+        assert not dm.value_free
+        T = pb.SparseMatrix(S.n_rows, S.n_cols, S.row_offsets, S.col_indices, np.asarray(S.values) * 0.5)
+        assert np.array_equal(plan.apply(th, 1, om), _oracle_embed(T, th, om))
+        dm.close()
+
+    def test_config2_full_size_on_off_identical(self):
+        # BASELINE config 2's graph: both dtypes, value-free on vs off bit-identical
+        # (heavy-row chunks none here; row order windows as in the bench)
+        S = graphs.sbm(1_000_000, 100, 15.0, 5.0, seed=2)
+        th = pb.legendre_coefficients(pb.indicator_above(0.95), 8).coeffs
+        for dt in ("float64", "float32"):
+            dm = pb.DeviceMatrix(S, dt)
+            assert dm.value_free
+            plan = dm.plan(80)
+            plan.set_option(_lib.OPT_VALUE_FREE, 1)
+            plan.run(th, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7)
+            a = _device_result(plan, 80)
+            plan.set_option(_lib.OPT_VALUE_FREE, 0)
+            plan.run(th, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7)
+            b = _device_result(plan, 80)
+            assert bool((a == b).all())
+            dm.close()
