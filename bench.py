@@ -106,15 +106,20 @@ class ClockSampler:
             if len(parts) < 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), parts[3:]))
+                try:
+                    pw = float(parts[2])
+                except ValueError:
+                    pw = None
+                rows.append((float(parts[0]), float(parts[1]), parts[3:], pw))
             except ValueError:
                 continue
         if not rows:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, p in rows for i, v in enumerate(p[1:5]) if v.lower() == "active"})
+        reasons = sorted({names[i] for _, _, p, _ in rows for i, v in enumerate(p[1:5]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "power_w": statistics.median(pw) if (pw := [r[3] for r in rows if r[3] is not None]) else None}
 
 
 def throttled(summary) -> bool:
@@ -210,7 +215,7 @@ def live_ceilings(ctx, row_bytes: int, q_bytes: int = 0):
     return out
 
 
-def gather_floor(dm, row_bytes: int, k1_ms: float):
+def gather_floor(dm, row_bytes: int, k1_ms: float, warm=None):
     """The same-data floor of K1, measured live next to the timed region:
     csemb_diag_gather_csr fetches, for every stored entry of THIS matrix in
     stored order, the whole row_bytes-wide row of a Q(r-1)-sized block -- K1's
@@ -224,13 +229,16 @@ def gather_floor(dm, row_bytes: int, k1_ms: float):
 
     best = None
     for depth in (4, 8):
+        if warm is not None:  # enqueue a whole embedding first: the probe runs right behind it, in the
+            warm()            # same (power-capped) clock state as the timed K1 launches
         ms, gbs = C.c_double(0.0), C.c_double(0.0)
         _lib.check(dm.lib.csemb_diag_gather_csr(dm.handle, row_bytes, depth, C.byref(ms), C.byref(gbs)),
                    "csemb_diag_gather_csr")
         if best is None or ms.value < best["ms"]:
             best = {"ms": round(ms.value, 4), "gathered_gbs": round(gbs.value, 1), "in_flight": depth}
     best["k1_over_floor"] = round(k1_ms / best["ms"], 3)
-    best["source"] = "csemb_diag_gather_csr (csrc/diag.cu): gather-only pass over the bench matrix, same clocks"
+    best["source"] = ("csemb_diag_gather_csr (csrc/diag.cu): gather-only pass over the bench matrix"
+                      + (", enqueued right behind a full embedding (same clock state)" if warm else ""))
     return best
 
 
@@ -376,7 +384,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         roof["gather"] = gather_roof(nnz, (hi - lo + W - 1) // W * W, dtype, k1_ms)
         roof["l2_fabric"] = fabric_roof(dm.ctx, nnz, n, hi - lo, (hi - lo + W - 1) // W * W, dtype, k1_ms, L)
         roof["l2_fabric"]["hbm_frac_of_live_copy"] = round(achieved / roof["l2_fabric"]["live_ceilings_gbs"]["hbm_copy"], 4)
-        roof["gather_floor"] = gather_floor(dm, (hi - lo + W - 1) // W * W * (8 if dtype == "f64" else 4), k1_ms)
+        roof["gather_floor"] = gather_floor(
+            dm, (hi - lo + W - 1) // W * W * (8 if dtype == "f64" else 4), k1_ms,
+            warm=lambda: plan.run(coeffs, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7, col0=lo, d_global=d,
+                                 normalize_rows=(world == 1)))  # the same E the downstream legs read
         if traffic:
             # K1 against HBM on its ACTUAL traffic (ncu bytes per launch over the live K1
             # time): between the live random-row ceiling (its gathers' misses) and the

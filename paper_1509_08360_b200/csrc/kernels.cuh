@@ -892,7 +892,6 @@ __device__ __forceinline__ bool omega_sign(int kind, uint64_t key, uint64_t seed
     return (r.x >> 31) != 0;
 }
 
-// Q(0) = block, E = theta0 * block; pad columns [d, ld) are zero.
 // Value-free detection: *ok stays 1 only if every stored value equals
 // vf_value(len(row), len(col)) bit for bit (one warp per row, lanes over its
 // entries); a zero-length column (1/sqrt(0) = inf) never matches a finite value.
@@ -914,6 +913,7 @@ __global__ void k_vf_check(const int64_t *__restrict__ rowptr, const int *__rest
     }
 }
 
+// Q(0) = block, E = theta0 * block; pad columns [d, ld) are zero.
 template <typename T>
 __global__ void k_stage_init(const double *__restrict__ given, T *y0, T *E, int64_t n, int d,
                              int ld, int kind, uint64_t seed, int64_t col0, int64_t d_global,
