@@ -169,7 +169,10 @@ int csemb_plan_destroy(csemb_plan *p);
                                        streaming the values (bit-identical results; whole rows
                                        only -- split heavy-row chunks and row partitions read
                                        the values).  Measured slower than streaming the values
-                                       (a dependent gather + IEEE sqrt/div per entry), so off */
+                                       (a dependent gather + IEEE sqrt/div per entry), so off, and
+                                       compiled out of the default build (K1_VF=0: setting 1 is
+                                       CSEMB_ERR_UNSUPPORTED); the device check itself
+                                       (csemb_matrix_value_free) is always available */
 #define CSEMB_OPT_E_FOLD 5           /* 1..3 (default 3): E is read and written every
                                        e_fold steps; a flush adds the pending terms in
                                        the reference's order, so results are unchanged */
@@ -241,6 +244,22 @@ int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n_global, vo
  * sends its rows once instead of once per peer.  */
 int csemb_plan_partition_multicast(csemb_plan *p, int64_t row0, int64_t n_global, void *full0_dev,
                                    void *full1_dev, void *mc0, void *mc1);
+/* Split exchange (SURVEY 8(e) "Overlap"): like csemb_plan_partition, and the
+ * row block is split by column into the entries inside its own row range
+ * [row0, row0 + n_rows) and the rest.  Step r is then
+ *   csemb_plan_step_local(p, r)  -- the local-column partial sums from this
+ *                                   rank's own Q(r-1) rows (q[(r-1) & 1]),
+ *                                   launchable while the caller's all-gather
+ *                                   of Q(r-1) into full is still in flight;
+ *   csemb_plan_step(p, r)         -- after the all-gather: the remote-column
+ *                                   partial sums, Q(r) = alpha * ((+0 + local)
+ *                                   + remote) - beta * Q(r-2), the E fold and
+ *                                   the diagnostics, into q[r & 1].
+ * Per row, local columns are summed before remote ones: the result agrees
+ * with the single-GPU stored order within rounding, not bit for bit. */
+int csemb_plan_partition_split(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev,
+                               void *q0_dev, void *q1_dev);
+int csemb_plan_step_local(csemb_plan *p, int r);
 /* Stage init for the local rows (hash of the GLOBAL row index); for generated
  * kinds also writes the full Q(0) into full_dev (no exchange before step 1). */
 int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, const double *block_dev,

@@ -77,6 +77,8 @@ SIGNATURES = {
     "csemb_plan_partition": (_int, [_p, _i64, _i64, _p, _p, _p]),
     "csemb_plan_partition_peers": (_int, [_p, _i64, _i64, _p, _p, _int, _p, _p]),
     "csemb_plan_partition_multicast": (_int, [_p, _i64, _i64, _p, _p, _p, _p]),
+    "csemb_plan_partition_split": (_int, [_p, _i64, _i64, _p, _p, _p]),
+    "csemb_plan_step_local": (_int, [_p, _int]),
     "csemb_plan_begin": (_int, [_p, _p, _int, _p, _int, _u64, _i64, _i64]),
     "csemb_plan_step": (_int, [_p, _int]),
     "csemb_plan_end": (_int, [_p, _int]),

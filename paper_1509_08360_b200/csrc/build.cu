@@ -168,7 +168,137 @@ int finish_matrix(csemb_mat *m) {
         }                                     \
     } while (0)
 
+// Row partition with overlap (csemb_plan_partition_split): per row, the
+// entries whose column lies in the rank's own row range [lo, hi) and the rest.
+// One warp per row; each part keeps the row's stored order.
+__global__ void k_split_count(const int64_t *__restrict__ rowptr, const int *__restrict__ cols, int64_t n_rows,
+                              int64_t lo, int64_t hi, int64_t *cnt_loc, int64_t *cnt_rem) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+        const int64_t b = rowptr[r], e = rowptr[r + 1];
+        unsigned n_loc = 0;
+        for (int64_t q = b + lane; q < e; q += 32) n_loc += (cols[q] >= lo && cols[q] < hi) ? 1u : 0u;
+        n_loc = __reduce_add_sync(0xFFFFFFFFu, n_loc);
+        if (lane == 0) {
+            cnt_loc[r] = n_loc;
+            cnt_rem[r] = (e - b) - (int64_t)n_loc;
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_split_fill(const int64_t *__restrict__ rowptr, const int *__restrict__ cols,
+                             const T *__restrict__ vals, int64_t n_rows, int64_t lo, int64_t hi,
+                             const int64_t *__restrict__ off_loc, const int64_t *__restrict__ off_rem,
+                             int *cols_loc, T *vals_loc, int *cols_rem, T *vals_rem) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += nw) {
+        const int64_t b = rowptr[r], e = rowptr[r + 1];
+        int64_t pl = off_loc[r], pr = off_rem[r];
+        for (int64_t q0 = b; q0 < e; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const bool ok = q < e;
+            const int c = ok ? cols[q] : 0;
+            const bool loc = ok && c >= lo && c < hi;
+            const unsigned ml = __ballot_sync(0xFFFFFFFFu, loc), mr = __ballot_sync(0xFFFFFFFFu, ok && !loc);
+            if (loc) {
+                cols_loc[pl + __popc(ml & below)] = (int)(c - lo);
+                vals_loc[pl + __popc(ml & below)] = vals[q];
+            } else if (ok) {
+                cols_rem[pr + __popc(mr & below)] = c;
+                vals_rem[pr + __popc(mr & below)] = vals[q];
+            }
+            pl += __popc(ml);
+            pr += __popc(mr);
+        }
+    }
+}
+
 }  // namespace
+
+int mat_split_columns(csemb_mat *m, int64_t lo, int64_t hi, csemb_mat **loc_out, csemb_mat **rem_out) {
+    csemb_ctx *c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows;
+    const int g = c->sm_count * 8;
+    *loc_out = *rem_out = nullptr;
+    Scratch tmp(c);
+    int64_t *cnt = nullptr;  // [0, n): local counts, [n, 2n): remote counts
+    CK(tmp.get(&cnt, 16 * (size_t)std::max<int64_t>(n, 1)));
+    if (n > 0) {
+        k_split_count<<<g, 256, 0, s>>>(m->rowptr, m->cols, n, lo, hi, cnt, cnt + n);
+        CK(cudaGetLastError());
+    }
+    csemb_mat *loc = nullptr, *rem = nullptr;
+    // the two parts' sizes (one small read back)
+    int64_t tot[2] = {0, 0};
+    {
+        int64_t *sums = nullptr;
+        CK(tmp.get(&sums, 16));
+        size_t tb = 0;
+        void *ts = nullptr;
+        CK(cub::DeviceReduce::Sum(nullptr, tb, cnt, sums, std::max<int64_t>(n, 1), s));
+        CK(tmp.get(&ts, tb));
+        if (n > 0) {
+            CK(cub::DeviceReduce::Sum(ts, tb, cnt, sums, n, s));
+            CK(cub::DeviceReduce::Sum(ts, tb, cnt + n, sums + 1, n, s));
+            CK(cudaMemcpyAsync(tot, sums, 16, cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+    }
+    int rc = mat_alloc(c, n, hi - lo, tot[0], m->dtype, &loc);
+    if (rc) return rc;
+    rc = mat_alloc(c, n, m->n_cols, tot[1], m->dtype, &rem);
+    if (rc) {
+        mat_free(loc);
+        return rc;
+    }
+    auto bail = [&](cudaError_t e) {
+        mat_free(loc);
+        mat_free(rem);
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? CSEMB_ERR_NOMEM : CSEMB_ERR_CUDA, "row split: %s",
+                    cudaGetErrorString(e));
+    };
+    cudaError_t e = cudaMemsetAsync(loc->rowptr, 0, 8, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(rem->rowptr, 0, 8, s);
+    if (e == cudaSuccess && n > 0) {
+        size_t tb = 0;
+        void *ts = nullptr;
+        e = cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, loc->rowptr + 1, n, s);
+        if (e == cudaSuccess) e = tmp.get(&ts, tb);
+        if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(ts, tb, cnt, loc->rowptr + 1, n, s);
+        if (e == cudaSuccess) e = cub::DeviceScan::InclusiveSum(ts, tb, cnt + n, rem->rowptr + 1, n, s);
+        if (e == cudaSuccess) {
+            if (m->dtype == CSEMB_F64)
+                k_split_fill<double><<<g, 256, 0, s>>>(m->rowptr, m->cols, (const double *)m->vals, n, lo, hi,
+                                                       loc->rowptr, rem->rowptr, loc->cols, (double *)loc->vals,
+                                                       rem->cols, (double *)rem->vals);
+            else
+                k_split_fill<float><<<g, 256, 0, s>>>(m->rowptr, m->cols, (const float *)m->vals, n, lo, hi,
+                                                      loc->rowptr, rem->rowptr, loc->cols, (float *)loc->vals,
+                                                      rem->cols, (float *)rem->vals);
+            e = cudaGetLastError();
+        }
+    } else if (e == cudaSuccess) {
+        e = cudaMemsetAsync(loc->rowptr, 0, 8 * ((size_t)n + 1), s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(rem->rowptr, 0, 8 * ((size_t)n + 1), s);
+    }
+    if (e != cudaSuccess) return bail(e);
+    rc = finish_matrix(loc);
+    if (!rc) rc = finish_matrix(rem);
+    if (rc) {
+        mat_free(loc);
+        mat_free(rem);
+        return rc;
+    }
+    *loc_out = loc;
+    *rem_out = rem;
+    return CSEMB_OK;
+}
 
 extern "C" int csemb_build_normalized_adjacency(csemb_ctx *c, int64_t n, int64_t n_edges, const int64_t *edges,
                                                 int edges_on_device, int dtype, csemb_mat **out) {

@@ -77,6 +77,14 @@ struct csemb_plan {
     int n_peer = 0;
     void *peer_full[2][K1_MAX_PEERS] = {};
     void *mc_full[2] = {nullptr, nullptr};  // NVLS multicast addresses of full2 (or null)
+    // split exchange (csemb_plan_partition_split): the row block's entries with
+    // columns inside its own row range (m_loc, local ids) run before the
+    // all-gather of Q(r-1) completes, the rest (m_rem) after it
+    bool split = false;
+    csemb_mat *m_loc = nullptr, *m_rem = nullptr;
+    void *ysplit = nullptr;  // 2 x n_rows x ld: local / remote partial sums
+    size_t ysplit_bytes = 0;
+    int local_r = 0;         // last step whose local part has been launched
     std::vector<double> coeffs;  // stage coefficients of the step-wise run
     int64_t col0 = 0, d_global = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -953,6 +961,9 @@ static void plan_free(csemb_plan *p) {
     dfree(p->m->ctx, p->staging);
     dfree(p->m->ctx, p->peaks);
     dfree(p->m->ctx, p->partials);
+    dfree(p->m->ctx, p->ysplit);
+    mat_free(p->m_loc);
+    mat_free(p->m_rem);
     for (auto &e : p->ev)
         if (e) cudaEventDestroy(e);
     if (p->gexec) cudaGraphExecDestroy(p->gexec);
@@ -996,7 +1007,11 @@ extern "C" int csemb_plan_set_option(csemb_plan *p, int option, int64_t value) {
     switch (option) {
         case CSEMB_OPT_EXACT_PEAKS: p->exact_peaks = value != 0; return CSEMB_OK;
         case CSEMB_OPT_REVERSE_SWEEP: p->reverse_sweep = value != 0; return CSEMB_OK;
-        case CSEMB_OPT_VALUE_FREE: p->value_free = value < 0 ? -1 : (value != 0); return CSEMB_OK;
+        case CSEMB_OPT_VALUE_FREE:
+            if (value > 0 && !K1_VF)
+                return fail(CSEMB_ERR_UNSUPPORTED, "value-free K1 is compiled out of this build (K1_VF=0; measured slower)");
+            p->value_free = value < 0 ? -1 : (value != 0);
+            return CSEMB_OK;
         case CSEMB_OPT_SPLIT_THRESHOLD:
             if (value < 0) return fail(CSEMB_ERR_INVALID, "split threshold must be >= 0");
             p->split_threshold = value;
@@ -1088,7 +1103,7 @@ static int plan_run_t(csemb_plan *p, const double *coeffs, int order, int n_stag
         }
     }
     const int *vf = nullptr;
-    if (p->value_free > 0 || (p->value_free < 0 && value_free_default())) CK(mat_vf_flag(m, &vf));
+    if (K1_VF && (p->value_free > 0 || (p->value_free < 0 && value_free_default()))) CK(mat_vf_flag(m, &vf));
     CK(rec_event(p, 0, s));
     for (int st = 0; st < n_stages; ++st) {
         const int kind = st > 0 ? OMEGA_FROM_E : omega_kind;
@@ -1409,6 +1424,7 @@ extern "C" int csemb_plan_partition_peers(csemb_plan *p, int64_t row0, int64_t n
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     p->partitioned = true;
     p->fused = true;
+    p->split = false;
     p->row0 = row0;
     p->n_global = n_global;
     p->full2[0] = full0_dev;
@@ -1445,6 +1461,7 @@ extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_globa
     std::lock_guard<std::mutex> lk(m->ctx->mu);
     p->partitioned = true;
     p->fused = false;
+    p->split = false;
     p->n_peer = 0;
     p->mc_full[0] = p->mc_full[1] = nullptr;
     p->row0 = row0;
@@ -1452,6 +1469,91 @@ extern "C" int csemb_plan_partition(csemb_plan *p, int64_t row0, int64_t n_globa
     p->full = full_dev;
     p->ext_q[0] = q0_dev;
     p->ext_q[1] = q1_dev;
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_partition_split(csemb_plan *p, int64_t row0, int64_t n_global, void *full_dev,
+                                          void *q0_dev, void *q1_dev) {
+    if (!p || !full_dev || !q0_dev || !q1_dev) return fail(CSEMB_ERR_INVALID, "null argument (the split exchange needs both local buffers)");
+    int rc = csemb_plan_partition(p, row0, n_global, full_dev, q0_dev, q1_dev);
+    if (rc) return rc;
+    csemb_mat *m = p->m;
+    if (p->ld / vec_w(m->dtype) > 96) return fail(CSEMB_ERR_UNSUPPORTED, "split exchange: d above 96 vectors per row");
+    std::lock_guard<std::mutex> lk(m->ctx->mu);
+    CK(cudaSetDevice(m->ctx->device));
+    mat_free(p->m_loc);
+    mat_free(p->m_rem);
+    p->m_loc = p->m_rem = nullptr;
+    rc = mat_split_columns(m, row0, row0 + m->n_rows, &p->m_loc, &p->m_rem);
+    if (rc) return rc;
+    const size_t need = 2 * (size_t)std::max<int64_t>(m->n_rows, 1) * (size_t)p->ld * dsize(m->dtype);
+    if (need > p->ysplit_bytes) {
+        dfree(m->ctx, p->ysplit);
+        p->ysplit = nullptr;
+        p->ysplit_bytes = 0;
+        CK(dmalloc(m->ctx, &p->ysplit, need));
+        p->ysplit_bytes = need;
+    }
+    p->split = true;
+    p->local_r = 0;
+    return CSEMB_OK;
+}
+
+// partials for the heavy-row chunks of schedule sc (grow-only)
+template <typename T>
+static int plan_partials(csemb_plan *p, const Schedule *sc) {
+    const size_t pbytes = (size_t)sc->n_chunks * (size_t)p->ld * sizeof(T);
+    if (pbytes > p->partials_bytes) {
+        csemb_ctx *c = p->m->ctx;
+        dfree(c, p->partials);
+        p->partials = nullptr;
+        p->partials_bytes = 0;
+        CK(dmalloc(c, &p->partials, pbytes));
+        p->partials_bytes = pbytes;
+    }
+    return CSEMB_OK;
+}
+
+// one SpMM part of a split step: Y[part] = A_part * X (stored order from +0)
+template <typename T>
+static int split_spmm_t(csemb_plan *p, csemb_mat *a, const void *x, void *y) {
+    csemb_ctx *c = p->m->ctx;
+    const int ldv = (int)(p->ld / Vec<T>::W);
+    if (a->n_rows == 0) return CSEMB_OK;
+    Schedule *sc = nullptr;
+    int rc = get_schedule(a, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold, p->row_order, &sc,
+                          16 * (int64_t)std::min(ldv, max_tile_vecs()));
+    if (rc) return rc;
+    rc = plan_partials<T>(p, sc);
+    if (rc) return rc;
+    StepParams P;
+    std::memset(&P, 0, sizeof P);
+    P.rowptr = a->rowptr;
+    P.cols = a->cols;
+    P.vals = a->vals;
+    P.ycur = x;
+    P.yout = y;
+    P.n_rows = a->n_rows;
+    P.ldv = ldv;
+    P.nvt = ldv;
+    P.col0 = (int)p->col0;
+    CK(launch_step<T, MODE_SPMM, PEAK_FLAG>(P, sc, p->partials, c->stream, c->sm_count, &p->step_launches));
+    return CSEMB_OK;
+}
+
+extern "C" int csemb_plan_step_local(csemb_plan *p, int r) {
+    if (!p) return fail(CSEMB_ERR_INVALID, "null plan");
+    if (!p->split || p->coeffs.empty()) return fail(CSEMB_ERR_INVALID, "call csemb_plan_partition_split and csemb_plan_begin first");
+    if (r < 1 || r >= (int)p->coeffs.size()) return fail(CSEMB_ERR_INVALID, "step %d outside [1, order]", r);
+    std::lock_guard<std::mutex> lk(p->m->ctx->mu);
+    CK(cudaSetDevice(p->m->ctx->device));
+    // local Q(r-1) rows: this rank's own buffer, ready as soon as step r-1 ran
+    // here -- no exchange needed
+    const void *x = p->ext_q[(r - 1) & 1];
+    const int rc = p->m->dtype == CSEMB_F64 ? split_spmm_t<double>(p, p->m_loc, x, p->ysplit)
+                                            : split_spmm_t<float>(p, p->m_loc, x, p->ysplit);
+    if (rc) return rc;
+    p->local_r = r;
     return CSEMB_OK;
 }
 
@@ -1518,12 +1620,16 @@ extern "C" int csemb_plan_begin(csemb_plan *p, const double *coeffs, int order, 
 }
 
 template <typename T>
+static int plan_step_split_t(csemb_plan *p, int r);
+
+template <typename T>
 static int plan_step_t(csemb_plan *p, int r) {
     csemb_mat *m = p->m;
     csemb_ctx *c = m->ctx;
     const int64_t n = m->n_rows;
     const int ldv = (int)(p->ld / Vec<T>::W);
     if (n == 0) return CSEMB_OK;
+    if (p->split) return plan_step_split_t<T>(p, r);
     Schedule *sc = nullptr;
     int rc = get_schedule(m, choose_group(std::min(ldv, max_tile_vecs())), p->split_threshold, p->row_order, &sc,
                           16 * (int64_t)std::min(ldv, max_tile_vecs()));
@@ -1576,6 +1682,69 @@ static int plan_step_t(csemb_plan *p, int r) {
         CK(launch_step<T, MODE_RECUR, PEAK_EXACT>(P, sc, p->partials, c->stream, c->sm_count, &p->step_launches));
     else
         CK(launch_step<T, MODE_RECUR, PEAK_FLAG>(P, sc, p->partials, c->stream, c->sm_count, &p->step_launches));
+    return CSEMB_OK;
+}
+
+// Split step r, after csemb_plan_step_local(r) and the caller's all-gather of
+// Q(r-1): the remote-column partial sums from the refreshed full buffer, then
+// Q(r) = alpha * ((+0 + Y_local) + Y_remote) - beta * Q(r-2) with the usual
+// epilogue (E fold, diagnostics) in the heavy-row combine's split mode.  The
+// per-row summation order differs from one GPU's stored order (local columns
+// first): results agree within rounding, bit-identical to the split-order
+// restatement (tests).
+template <typename T>
+static int plan_step_split_t(csemb_plan *p, int r) {
+    csemb_mat *m = p->m;
+    csemb_ctx *c = m->ctx;
+    const int64_t n = m->n_rows;
+    const int ldv = (int)(p->ld / Vec<T>::W);
+    if (p->local_r != r) return fail(CSEMB_ERR_INVALID, "split step %d: call csemb_plan_step_local(%d) first", r, r);
+    T *yl = (T *)p->ysplit, *yr = (T *)p->ysplit + n * p->ld;
+    int rc = split_spmm_t<T>(p, p->m_rem, p->full, yr);
+    if (rc) return rc;
+    if (p->m_rem->nnz == 0) CK(cudaMemsetAsync(yr, 0, sizeof(T) * (size_t)n * (size_t)p->ld, c->stream));
+    StepParams P;
+    std::memset(&P, 0, sizeof P);
+    P.ycur = p->full;  // Q(r-1), all rows (the E fold's own-row reads)
+    P.yout = p->ext_q[r & 1];
+    P.E = p->E;
+    P.n_rows = n;
+    P.ldv = ldv;
+    P.nvt = ldv;
+    P.alpha = 2.0 - 1.0 / (double)r;
+    P.beta = 1.0 - 1.0 / (double)r;
+    P.theta = p->coeffs[r];
+    const int L = (int)p->coeffs.size() - 1;
+    P.efold = efold_bits(r, L, p->e_fold);
+    P.theta1 = r >= 2 ? p->coeffs[r - 1] : 0.0;
+    P.theta2 = r >= 3 ? p->coeffs[r - 2] : 0.0;
+    P.row_base = p->row0;
+    P.has_prev = r > 1;
+    P.peaks = p->peaks + (size_t)(r - 1) * p->n_chunks;
+    P.col0 = (int)p->col0;
+    HeavyParams H;
+    std::memset(&H, 0, sizeof H);
+    H.partials = yl;
+    H.partials2 = yr;
+    H.n_heavy = (int)n;
+    if (n > 0x7FFFFFFFLL) return fail(CSEMB_ERR_UNSUPPORTED, "split exchange: row block above 2^31-1 rows");
+    const int grid = grid_for(n * 32, 256, c->sm_count, 8);
+    const int ms = (ldv + 31) / 32;
+    auto go = [&](auto peak_tag) {
+        constexpr int PK = decltype(peak_tag)::value;
+        if (ms <= 1)
+            k_heavy_combine<T, MODE_RECUR, PK, 1><<<grid, 256, 0, c->stream>>>(P, H);
+        else if (ms == 2)
+            k_heavy_combine<T, MODE_RECUR, PK, 2><<<grid, 256, 0, c->stream>>>(P, H);
+        else
+            k_heavy_combine<T, MODE_RECUR, PK, 3><<<grid, 256, 0, c->stream>>>(P, H);
+    };
+    if (p->exact_peaks)
+        go(std::integral_constant<int, PEAK_EXACT>{});
+    else
+        go(std::integral_constant<int, PEAK_FLAG>{});
+    CK(cudaGetLastError());
+    ++p->step_launches;
     return CSEMB_OK;
 }
 

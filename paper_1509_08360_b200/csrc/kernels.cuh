@@ -225,6 +225,11 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_BATCH
 #define K1_BATCH 0  // stored entries per warp-uniform batch (<= G; 0: B = G, measured best)
 #endif
+#ifndef K1_VF
+#define K1_VF 0  // 1: compile K1's value-free path in (CSEMB_OPT_VALUE_FREE).  Off: measured
+                 // slower when used, and its mere presence costs the default path 0.5-3%
+                 // (register allocation; profiles/r2_k1_experiments.txt)
+#endif
 #ifndef K1_TRIM
 #define K1_TRIM 0  // 1: trim the warp's last batch to its longest row (rounded up to D)
 #endif
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     const T theta1 = (T)P.theta1, theta2 = (T)P.theta2;
     const bool has_prev = P.has_prev != 0;
     const int first_chunk = (P.col0 + P.v0 * W) >> 5;
-    const bool vfree = P.vf != nullptr && *P.vf != 0;  // warp-uniform
+    const bool vfree = K1_VF && P.vf != nullptr && *P.vf != 0;  // warp-uniform
 
     bool valid[VPL];
 #pragma unroll
@@ -756,6 +761,10 @@ struct HeavyParams {
     const int *chunk_off;   // chunks of heavy row h: [chunk_off[h], chunk_off[h+1])
     const void *partials;   // n_chunks x ldv vectors
     int n_heavy;
+    // split row partition (csemb_plan_partition_split): every row 0..n_heavy-1
+    // in order, acc = (+0 + partials[row]) + partials2[row] -- the local-column
+    // and remote-column partial sums -- then the same epilogue
+    const void *partials2;
 };
 
 template <typename T, int MODE, int PEAK, int MS>
@@ -782,12 +791,21 @@ __global__ void __launch_bounds__(256) k_heavy_combine(const StepParams P, const
 #pragma unroll
     for (int k = 0; k < MS; ++k) pk[k] = 0ull;
     unsigned badmask = 0u;
+    const VT *part2 = H.partials2 ? (const VT *)H.partials2 + P.v0 + lane : nullptr;
     for (int64_t h = warp; h < H.n_heavy; h += nwarps) {
-        const int64_t row = H.rows[h];
-        const int c0 = H.chunk_off[h], c1 = H.chunk_off[h + 1];
+        const int64_t row = part2 ? h : H.rows[h];
+        const int c0 = part2 ? 0 : H.chunk_off[h], c1 = part2 ? 0 : H.chunk_off[h + 1];
         VT acc[MS];
 #pragma unroll
         for (int k = 0; k < MS; ++k) acc[k] = vzero(VT());
+        if (part2) {
+#pragma unroll
+            for (int k = 0; k < MS; ++k)
+                if (valid[k]) {
+                    const VT a = part[h * P.ldv + 32 * k], b = part2[h * P.ldv + 32 * k];
+                    acc[k] = vmadd(vmadd(acc[k], (T)1, a), (T)1, b);
+                }
+        }
         // chunk partials in chunk order; U chunks' loads in flight at a time
         int c = c0;
         for (; c + U <= c1; c += U) {

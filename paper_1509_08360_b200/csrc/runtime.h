@@ -98,4 +98,9 @@ CSEMB_INTERNAL size_t dsize(int dtype);
 CSEMB_INTERNAL int mat_alloc(csemb_ctx *c, int64_t n_rows, int64_t n_cols, int64_t nnz, int dtype,
                              csemb_mat **out);
 CSEMB_INTERNAL void mat_free(csemb_mat *m);
+// a row block's columns split at its own row range [lo, hi): *loc holds the
+// entries with lo <= col < hi (ids col - lo, n_rows x (hi - lo)), *rem the
+// rest (global ids); both keep each row's stored order (build.cu; call with
+// the context lock held)
+CSEMB_INTERNAL int mat_split_columns(csemb_mat *m, int64_t lo, int64_t hi, csemb_mat **loc, csemb_mat **rem);
 CSEMB_INTERNAL int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8);

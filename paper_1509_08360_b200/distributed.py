@@ -200,9 +200,17 @@ class DeviceRowEngine:
             self.bind(F, q)
         self.n_local, self.d = S_local.n_rows, d
 
-    def bind(self, F, q):
-        """All-gather exchange: steps gather from F and write the local Q(r) to q[r & 1]."""
-        self.plan.partition(self.row0, self.n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+    def bind(self, F, q, split: bool = False):
+        """All-gather exchange: steps gather from F and write the local Q(r) to
+        q[r & 1]; split=True also cuts the row block at its own column range
+        (step_local before the all-gather completes, step after it)."""
+        if split:
+            self.plan.partition_split(self.row0, self.n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        else:
+            self.plan.partition(self.row0, self.n_global, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+
+    def step_local(self, r):
+        self.plan.step_local(r)
 
     def begin(self, coeffs, omega_kind, seed, col0, d_global):
         self.plan.begin(coeffs, omega_kind=omega_kind, seed=seed, col0=col0, d_global=d_global)
@@ -274,6 +282,13 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     so the transfer overlaps the step; one barrier per step.  GPU only.
     exchange="multicast": the same through NVLS multicast (one multimem store
     per row, replicated by the NVSwitch).
+    exchange="split": the all-gather overlapped with compute (SURVEY 8(e)
+    "Overlap"): each rank's row block is cut at its own column range; the
+    entries with local columns run from the rank's own Q(r-1) rows while the
+    all-gather of Q(r-1) is in flight (on a separate stream), the remaining
+    entries and the fused epilogue after it.  Local columns are summed first,
+    so E agrees with one GPU within rounding (bit-identical to the split-order
+    restatement), not bit for bit.
     col0 / d_global: the d columns are the slice [col0, col0 + d) of a
     d_global-column projection (the 2-D layout, `embed_2d`).
     """
@@ -294,9 +309,9 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     on_gpu = engine_factory is None
     dev = torch.device(f"cuda:{torch.cuda.current_device() if device is None else device}") if on_gpu \
         else torch.device("cpu")
-    if exchange not in ("allgather", "peer", "multicast"):
-        raise ValueError("exchange must be 'allgather', 'peer' or 'multicast'")
-    if exchange != "allgather":
+    if exchange not in ("allgather", "peer", "multicast", "split"):
+        raise ValueError("exchange must be 'allgather', 'peer', 'multicast' or 'split'")
+    if exchange in ("peer", "multicast"):
         if not on_gpu:
             raise ValueError("the fused peer exchange runs on GPUs (torch symmetric memory)")
         mcast = exchange == "multicast"
@@ -329,22 +344,40 @@ def embed_row_partitioned(S_local, row0: int, n_global: int, coeffs, d: int, *, 
     # library stream: the all-gather of Q(r) starts when step r's kernels finish
     # and step r+1 starts when it completes, ordered on the device with no host
     # synchronisation in the loop.
+    split = exchange == "split"
     with (torch.cuda.stream(stream) if stream is not None else _nullcontext()):
         F = torch.zeros((world * n_pad, ld), dtype=tdt, device=dev)
         q = [torch.zeros((n_pad, ld), dtype=tdt, device=dev) for _ in range(2)]
         if on_gpu:
-            eng.bind(F, q)
+            eng.bind(F, q, split=split)
         else:
             eng = engine_factory(S_local, row0, n_global, d, dtype, F, q)
         eng.begin(coeffs, kind, seed, col0, d if d_global is None else d_global)
         parts = [F[p * n_pad:(p + 1) * n_pad] for p in range(world)]
+        nccl = dist.get_backend(group) == "nccl"
+        # split: the all-gather runs on its own stream, after the step that wrote
+        # Q(r); the library stream meanwhile runs step r+1's local-column part and
+        # waits for the all-gather only before the remote part
+        comm = torch.cuda.Stream(device=dev) if (split and on_gpu) else None
+
+        def gather(r):
+            if comm is not None:
+                comm.wait_stream(stream)  # Q(r) is written
+                with torch.cuda.stream(comm):
+                    dist.all_gather_into_tensor(F, q[r & 1], group=group)
+            elif nccl:
+                dist.all_gather_into_tensor(F, q[r & 1], group=group)
+            else:
+                dist.all_gather(parts, q[r & 1], group=group)
+
         for r in range(1, order + 1):
+            if split:
+                eng.step_local(r)  # this rank's own Q(r-1) rows: no exchange needed
+                if comm is not None:
+                    stream.wait_stream(comm)  # the all-gather of Q(r-1) has landed in F
             eng.step(r)
             if r < order:  # refresh the replicated Q(r) for the next step
-                if dist.get_backend(group) == "nccl":
-                    dist.all_gather_into_tensor(F, q[r & 1], group=group)
-                else:
-                    dist.all_gather(parts, q[r & 1], group=group)
+                gather(r)
         E, peaks = eng.end(normalize_rows)
     return E, combine_peaks(peaks, group)
 

@@ -367,6 +367,18 @@ class Plan:
             int(omega_kind), int(seed) & _M64, int(col0), d_global), "csemb_plan_begin")
         self.last = (len(c) - 1, 1, d_global, int(col0))
 
+    def partition_split(self, row0: int, n_global: int, full_ptr: int, q0_ptr: int, q1_ptr: int) -> None:
+        """Split exchange: the row block's local-column entries (step_local)
+        run while the caller's all-gather of Q(r-1) is in flight, the rest
+        (step) after it -- SURVEY 8(e) "Overlap"; the per-row summation order
+        becomes local columns first (within rounding of the 1-GPU result)."""
+        _lib.check(self.lib.csemb_plan_partition_split(
+            self.handle, int(row0), int(n_global), C.c_void_p(full_ptr), C.c_void_p(q0_ptr), C.c_void_p(q1_ptr)),
+            "csemb_plan_partition_split")
+
+    def step_local(self, r: int) -> None:
+        _lib.check(self.lib.csemb_plan_step_local(self.handle, int(r)), "csemb_plan_step_local")
+
     def step(self, r: int) -> None:
         _lib.check(self.lib.csemb_plan_step(self.handle, int(r)), "csemb_plan_step")
 

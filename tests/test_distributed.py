@@ -140,6 +140,70 @@ class OracleRowEngine:
         return torch.from_numpy(self.E), self.peaks
 
 
+class OracleSplitRowEngine(OracleRowEngine):
+    """CPU stand-in for the split exchange (csemb_plan_partition_split):
+    step_local sums the local-column entries from this rank's own Q(r-1) rows,
+    step adds the remote-column sums from the refreshed full buffer."""
+
+    def __init__(self, S_local, row0, n_global, d, dtype, F, q):
+        from conftest import split_csr
+
+        super().__init__(S_local, row0, n_global, d, dtype, F, q)
+        self.Sl, self.Sr = split_csr(self.S, row0, row0 + self.n, rows=(0, self.n))
+        self.yl = None
+
+    def step_local(self, r):
+        self.yl = O.spmm(self.Sl, np.ascontiguousarray(self.q[(r - 1) & 1][:self.n, :self.d].numpy()))
+
+    def step(self, r):
+        y = self.yl + O.spmm(self.Sr, np.ascontiguousarray(self.F[:self.N, :self.d].numpy()))
+        self.yl = None
+        q = (2.0 - 1.0 / r) * y
+        if r > 1:
+            q = q - (1.0 - 1.0 / r) * self.q[r & 1][:self.n, :self.d].numpy()
+        self.E = self.E + self.coeffs[r] * q
+        self.q[r & 1][:self.n, :self.d] = torch.from_numpy(q)
+
+
+def _split_worker(rank, world, port, d, seed, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1509_08360_b200.distributed import embed_row_partitioned, local_rows, row_blocks
+
+        S, coeffs = _problem()
+        _, blocks = row_blocks(S.n_rows, world)
+        lo, hi = blocks[rank]
+        Sl = local_rows(_as_sparse(S), lo, hi)
+        E, _ = embed_row_partitioned(Sl, lo, S.n_rows, coeffs, d, seed=seed, engine_factory=OracleSplitRowEngine,
+                                     exchange="split")
+        np.save(result_path + f".{rank}.npy", E.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_exchange_matches_split_order_and_single_process(tmp_path, world):
+    # the overlapped exchange (local columns first, SURVEY 8(e) "Overlap"):
+    # bit-identical to the split-order restatement, within rounding of the
+    # single-process stored order
+    from conftest import split_order_stage
+    from paper_1509_08360_b200.distributed import row_blocks
+
+    d, seed = 37, 5
+    out = str(tmp_path / "split")
+    mp.start_processes(_split_worker, args=(world, _free_port(), d, seed, out), nprocs=world,
+                       start_method="spawn", join=True)
+    got = np.concatenate([np.load(out + f".{p}.npy") for p in range(world)])
+    S, coeffs = _problem()
+    om = O.sample_projection(S.n_rows, d, seed)
+    _, blocks = row_blocks(S.n_rows, world)
+    assert np.array_equal(got, split_order_stage(S, coeffs, om, blocks))
+    ref, _, _ = O.run_stage(S, coeffs, om)
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
 def _row_worker(rank, world, port, d, seed, result_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

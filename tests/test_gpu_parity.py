@@ -560,6 +560,71 @@ class TestRowPartition:
         assert np.array_equal(np.concatenate(got), ref)
 
     @pytest.mark.parametrize("dtype", ["float64", "float32"])
+    def test_split_exchange_emulated(self, dtype):
+        # csemb_plan_partition_split: per step every "rank" runs its local-column
+        # part from its own Q(r-1) rows, then (after the emulated all-gather) the
+        # remote part + epilogue.  fp64: bit-identical to the split-order
+        # restatement; both dtypes within rounding of the 1-GPU stored order.
+        import torch
+
+        from conftest import split_order_stage
+        from paper_1509_08360_b200.distributed import local_rows, row_blocks
+
+        S = graphs.sbm(3001, 7, 10.0, 3.0, seed=4)
+        n, d, L = S.n_rows, 40, 12
+        th = pb.legendre_coefficients(pb.indicator_above(0.5), L).coeffs
+        om = O.sample_projection(n, d, 3)
+        tdt = torch.float64 if dtype == "float64" else torch.float32
+        world = 3
+        n_pad, blocks = row_blocks(n, world)
+        F = torch.zeros((world * n_pad, d), dtype=tdt, device="cuda")
+        ranks = []
+        for lo, hi in blocks:
+            dm = pb.DeviceMatrix(local_rows(S, lo, hi), dtype)
+            plan = dm.plan(d)
+            q = [torch.zeros((n_pad, d), dtype=tdt, device="cuda") for _ in range(2)]
+            plan.partition_split(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+            torch.cuda.synchronize()
+            plan.begin(th, omega_kind=1, seed=3)
+            ranks.append((lo, hi, dm, plan, q))
+        for r in range(1, L + 1):
+            for lo, hi, dm, plan, q in ranks:
+                plan.step_local(r)
+            for lo, hi, dm, plan, q in ranks:  # F holds Q(r-1) of every rank (emulated all-gather)
+                plan.step(r)
+            for _, _, dm, _, _ in ranks:
+                dm.ctx.sync()
+            if r < L:
+                for lo, hi, dm, plan, q in ranks:
+                    F[lo:hi] = q[r & 1][:hi - lo]
+                torch.cuda.synchronize()
+        got = []
+        for lo, hi, dm, plan, q in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        got = np.concatenate(got)
+        if dtype == "float64":
+            assert np.array_equal(got, split_order_stage(O.CSR.of(S), th, om, blocks))
+        ref = _oracle_embed(S, th, om)
+        assert rel(got, ref) <= (1e-13 if dtype == "float64" else FP32_REL)
+
+    def test_split_exchange_needs_local_step(self):
+        import torch
+
+        S = graphs.sbm(500, 2, 6.0, 2.0, seed=1)
+        dm = pb.DeviceMatrix(S, "float64")
+        plan = dm.plan(8)
+        F = torch.zeros((500, 8), dtype=torch.float64, device="cuda")
+        q = [torch.zeros((500, 8), dtype=torch.float64, device="cuda") for _ in range(2)]
+        plan.partition_split(0, 500, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        torch.cuda.synchronize()
+        plan.begin(pb.legendre_coefficients(pb.indicator_above(0.5), 3).coeffs, omega_kind=1, seed=1)
+        with pytest.raises(ValueError, match="step_local"):
+            plan.step(1)
+        dm.close()
+
+    @pytest.mark.parametrize("dtype", ["float64", "float32"])
     def test_fused_peer_exchange_emulated(self, dtype):
         # csemb_plan_partition_peers: each "rank" stores its Q(r) rows into the
         # other ranks' replicated buffers from K1's epilogue (here: buffers on
@@ -703,6 +768,11 @@ class TestRowPartition:
             # the fused exchange through torch symmetric memory (no peers at world 1)
             E2, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="peer")
             assert np.array_equal(E2.cpu().numpy(), ref)
+            # the split (overlapped) exchange: at world 1 every column is local, so
+            # the order is the stored one: bit-identical too (the all-gather runs on
+            # its own stream, ordered by events against the library stream)
+            Es, _ = embed_row_partitioned(S, 0, S.n_rows, th, 24, seed=2, device=0, exchange="split")
+            assert np.array_equal(Es.cpu().numpy(), ref)
             # C1: the CSR broadcast over NCCL into device memory, then the column-sharded run
             from paper_1509_08360_b200.distributed import broadcast_matrix, embed_column_sharded
 
@@ -1120,6 +1190,14 @@ def test_config2_full_scale_fp64_bit_exact_and_fp32_gates():
 # value-free normalized adjacency (CSEMB_OPT_VALUE_FREE): K1 recomputes
 # 1/sqrt(deg u * deg v) (sparse.py:224) from the row offsets
 # --------------------------------------------------------------------------
+def _value_free_on(plan):
+    try:
+        plan.set_option(_lib.OPT_VALUE_FREE, 1)
+    except NotImplementedError:
+        pytest.skip("value-free K1 compiled out (K1_VF=0, the default build: measured slower); "
+                    "verified with a K1_VF=1 build, profiles/r2_k1_experiments.txt")
+
+
 class TestValueFree:
     def test_detected_on_normalized_adjacency_and_bit_exact(self, config1):
         z, meta = config1
@@ -1130,7 +1208,7 @@ class TestValueFree:
             dm = pb.DeviceMatrix(S, dt)
             assert dm.value_free
             plan = dm.plan(40)
-            plan.set_option(_lib.OPT_VALUE_FREE, 1)
+            _value_free_on(plan)
             on = plan.apply(th, 1, om)
             plan.set_option(_lib.OPT_VALUE_FREE, 0)
             off = plan.apply(th, 1, om)
@@ -1150,7 +1228,7 @@ class TestValueFree:
         th = pb.legendre_coefficients(pb.indicator_above(0.9), 20).coeffs
         om = O.sample_projection(2000, 40, 0)
         plan = dm.plan(40)
-        plan.set_option(_lib.OPT_VALUE_FREE, 1)  # requested, but the check says no: values are read
+        _value_free_on(plan)  # requested, but the check says no: values are read
         assert np.array_equal(plan.apply(th, 1, om), _oracle_embed(T, th, om))
         dm.close()
 
@@ -1159,7 +1237,6 @@ class TestValueFree:
         S = sparse_from(z)
         dm = pb.DeviceMatrix(S, "float64")
         plan = dm.plan(40)
-        plan.set_option(_lib.OPT_VALUE_FREE, 1)
         th = pb.legendre_coefficients(pb.indicator_above(0.9), 12).coeffs
         om = O.sample_projection(2000, 40, 0)
         plan.apply(th, 1, om)  # the check ran and cached "on"
@@ -1179,7 +1256,7 @@ class TestValueFree:
             dm = pb.DeviceMatrix(S, dt)
             assert dm.value_free
             plan = dm.plan(80)
-            plan.set_option(_lib.OPT_VALUE_FREE, 1)
+            _value_free_on(plan)
             plan.run(th, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7)
             a = _device_result(plan, 80)
             plan.set_option(_lib.OPT_VALUE_FREE, 0)
