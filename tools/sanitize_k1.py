@@ -37,3 +37,38 @@ for dt in ("float64", "float32"):
     print(dt, "norm", dm.spectral_norm(5, 20, 1))
     dm.close()
 print("ok")
+
+# round 2: the split exchange (device column split + split combine), the
+# value-free check and the same-data gather floor
+import ctypes as C  # noqa: E402
+
+import torch  # noqa: E402
+
+from paper_1509_08360_b200 import _lib  # noqa: E402
+from paper_1509_08360_b200.distributed import local_rows, row_blocks  # noqa: E402
+
+for dt, tdt in (("float64", torch.float64), ("float32", torch.float32)):
+    world, d = 3, 40
+    n_pad, blocks = row_blocks(n, world)
+    F = torch.zeros((world * n_pad, d), dtype=tdt, device="cuda")
+    for lo, hi in blocks:
+        dm = pb.DeviceMatrix(local_rows(S, lo, hi), dt)
+        plan = dm.plan(d)
+        q = [torch.zeros((n_pad, d), dtype=tdt, device="cuda") for _ in range(2)]
+        plan.partition_split(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+        torch.cuda.synchronize()
+        plan.begin(th, omega_kind=1, seed=3)
+        for r in range(1, len(th)):
+            plan.step_local(r)
+            plan.step(r)
+        plan.end(True)
+        assert np.all(np.isfinite(plan.download()))
+        dm.close()
+    dm = pb.DeviceMatrix(S, dt)
+    print(dt, "value_free", dm.value_free)
+    for depth in (4, 8):
+        ms, gbs = C.c_double(), C.c_double()
+        _lib.check(dm.lib.csemb_diag_gather_csr(dm.handle, 80 * (8 if dt == "float64" else 4), depth,
+                                                C.byref(ms), C.byref(gbs)), "floor")
+    dm.close()
+print("ok (round 2 paths)")
