@@ -219,6 +219,10 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #ifndef K1_DEPTH
 #define K1_DEPTH 0  // stored entries in flight per lane (divides G); 0: 4 for fp64, 2 for fp32
 #endif
+#ifndef K1_DEPTH_F64_SPILLY
+#define K1_DEPTH_F64_SPILLY 2  // fp64 depth for the shapes that spill at 4 (4-lane groups, 32-lane SpMM, exact
+                                // peaks): spill-free at 2; measured 1-1.6% faster at d = 20 / 24 (round 2)
+#endif
 #ifndef K1_DEPTH_F32
 #define K1_DEPTH_F32 2  // fp32 entries in flight per lane (divides the batch)
 #endif
@@ -450,7 +454,11 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     // neighbour's row tile into a warp-private S-stage shared-memory ring; the
     // group waits on the stage's mbarrier and consumes it from shared memory.
     // VPL > 3 (K1_WIDE_VPL builds): the register budget allows only 2 entries in flight
-    constexpr int DEPTH = K1_DEPTH ? K1_DEPTH : (VPL > 3 ? 2 : (sizeof(T) == 8 ? 4 : K1_DEPTH_F32));
+    constexpr int DEPTH = K1_DEPTH ? K1_DEPTH
+                                   : (VPL > 3 ? 2
+                                              : (sizeof(T) == 8 ? ((G == 4 || (G == 32 && MODE == MODE_SPMM) || PEAK == PEAK_EXACT)
+                                                                       ? K1_DEPTH_F64_SPILLY : 4)
+                                                                : K1_DEPTH_F32));
     constexpr int D = STAGED ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
     // STAGED == 2: per-lane ring of D entries x VPL 16-byte slots in shared memory
     VT *lring = nullptr;
