@@ -609,6 +609,60 @@ class TestRowPartition:
         ref = _oracle_embed(S, th, om)
         assert rel(got, ref) <= (1e-13 if dtype == "float64" else FP32_REL)
 
+    @pytest.mark.parametrize("split_threshold", [0, None])
+    def test_split_exchange_heavy_rows(self, split_threshold):
+        # a power-law graph plus a 6000-entry hub row: heavy rows in both column
+        # parts (chunked SpMM + combine inside each part).  Strict stored order
+        # (threshold 0): bit-identical to the split-order restatement; default
+        # chunking: within rounding.
+        import torch
+
+        from conftest import split_order_stage
+        from paper_1509_08360_b200.distributed import local_rows, row_blocks
+
+        rng = np.random.default_rng(0)
+        n = 30011
+        e = np.concatenate([graphs.chung_lu_edges(n, seed=1),
+                            np.stack([np.full(6000, 7, np.int64), rng.integers(0, n, 6000)], 1)])
+        S = pb.normalized_adjacency(e, n)
+        d, L = 24, 8
+        th = pb.legendre_coefficients(pb.commute_time(0.01), L).coeffs
+        om = O.sample_projection(n, d, 3)
+        world = 3
+        n_pad, blocks = row_blocks(n, world)
+        F = torch.zeros((world * n_pad, d), dtype=torch.float64, device="cuda")
+        ranks = []
+        for lo, hi in blocks:
+            dm = pb.DeviceMatrix(local_rows(S, lo, hi), "float64")
+            plan = dm.plan(d)
+            if split_threshold is not None:
+                plan.set_load_balance(split_threshold=split_threshold)
+            q = [torch.zeros((n_pad, d), dtype=torch.float64, device="cuda") for _ in range(2)]
+            plan.partition_split(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+            torch.cuda.synchronize()
+            plan.begin(th, omega_kind=1, seed=3)
+            ranks.append((lo, hi, dm, plan, q))
+        for r in range(1, L + 1):
+            for *_, plan, _ in ranks:
+                plan.step_local(r)
+            for *_, plan, _ in ranks:
+                plan.step(r)
+            for _, _, dm, _, _ in ranks:
+                dm.ctx.sync()
+            if r < L:
+                for lo, hi, dm, plan, q in ranks:
+                    F[lo:hi] = q[r & 1][:hi - lo]
+                torch.cuda.synchronize()
+        got = []
+        for lo, hi, dm, plan, q in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        got = np.concatenate(got)
+        if split_threshold == 0:
+            assert np.array_equal(got, split_order_stage(O.CSR.of(S), th, om, blocks))
+        assert rel(got, _oracle_embed(S, th, om)) <= 1e-13
+
     def test_split_exchange_needs_local_step(self):
         import torch
 
