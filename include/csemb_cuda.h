@@ -94,7 +94,9 @@ int csemb_matrix_download_values(csemb_mat *m, double *values_out);
 /* a copy of m in another arithmetic type (values converted; CSR shared shape) */
 int csemb_matrix_convert(csemb_mat *m, int dtype, csemb_mat **out);
 /* borrowed device pointers of m's arrays (int64 offsets, int32 column ids,
- * values in m's dtype); valid until csemb_matrix_destroy(m) */
+ * values in m's dtype); valid until csemb_matrix_destroy(m).  Read-only:
+ * the library caches properties of the arrays (schedules, the value-free
+ * check); change values only through csemb_matrix_scale */
 int csemb_matrix_device_arrays(csemb_mat *m, void **row_offsets, void **col_indices, void **values);
 
 /* ---- measurement probes (bench.py roofline objects; not the embedding path) ----
