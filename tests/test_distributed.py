@@ -295,6 +295,10 @@ def _grid_worker(rank, world, port, grid, d, seed, result_path):
         np.save(result_path + f".{rank}.npy", E.numpy())
         En, _ = embed_2d(_as_sparse(S), coeffs, d, grid, seed=seed, engine_factory=OracleRowEngine, groups=groups)
         np.save(result_path + f".{rank}.norm.npy", En.numpy())
+        # the split (overlapped) exchange through the grid driver
+        Es, _ = embed_2d(_as_sparse(S), coeffs, d, grid, seed=seed, engine_factory=OracleSplitRowEngine,
+                         normalize_rows=False, groups=groups, exchange="split")
+        np.save(result_path + f".{rank}.split.npy", Es.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -316,6 +320,12 @@ def test_2d_grid_matches_single_process(tmp_path, grid):
         assert np.array_equal(np.load(out + f".{rank}.npy"), ref[lo:hi])  # every rank: its rows, all columns
         np.testing.assert_allclose(np.load(out + f".{rank}.norm.npy"), O.row_normalize(ref)[lo:hi], rtol=0,
                                    atol=1e-15)
+    from conftest import split_order_stage
+
+    split_ref = split_order_stage(S, coeffs, O.sample_projection(S.n_rows, d, seed), blocks)
+    for rank in range(world):
+        lo, hi = blocks[rank // grid[1]]
+        assert np.array_equal(np.load(out + f".{rank}.split.npy"), split_ref[lo:hi])
 
 
 def test_grid_shape_must_match_world(tmp_path):
