@@ -215,7 +215,7 @@ def live_ceilings(ctx, row_bytes: int, q_bytes: int = 0):
     return out
 
 
-def gather_floor(dm, row_bytes: int, k1_ms: float, warm=None):
+def gather_floor(dm, row_bytes: int, k1_ms: float, warm=None, ncu_dtype=None):
     """The same-data floor of K1, measured live next to the timed region:
     csemb_diag_gather_csr fetches, for every stored entry of THIS matrix in
     stored order, the whole row_bytes-wide row of a Q(r-1)-sized block -- K1's
@@ -237,6 +237,19 @@ def gather_floor(dm, row_bytes: int, k1_ms: float, warm=None):
         if best is None or ms.value < best["ms"]:
             best = {"ms": round(ms.value, 4), "gathered_gbs": round(gbs.value, 1), "in_flight": depth}
     best["k1_over_floor"] = round(k1_ms / best["ms"], 3)
+    try:  # config 2: the committed ncu captures of both kernels, time ratio vs DRAM-byte ratio
+        if ncu_dtype is None:
+            raise KeyError
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            t = json.load(fh)
+        fl, k1b, k1t = t["floor"][ncu_dtype], t[ncu_dtype], t["k1_ms"][ncu_dtype]
+        best["ncu"] = {"k1_over_floor_time": round(k1t / fl["ms"], 3),
+                       "k1_over_floor_dram_bytes": round(k1b / fl["dram_bytes"], 3),
+                       "k1_dram_tbs": round(k1b / (k1t * 1e-3) / 1e12, 2),
+                       "floor_dram_tbs": round(fl["dram_bytes"] / (fl["ms"] * 1e-3) / 1e12, 2),
+                       "source": "profiles/k1_traffic.json (config 2, full clock)"}
+    except (OSError, KeyError, ValueError):
+        pass
     best["source"] = ("csemb_diag_gather_csr (csrc/diag.cu): gather-only pass over the bench matrix"
                       + (", enqueued right behind a full embedding (same clock state)" if warm else ""))
     return best
@@ -387,7 +400,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         roof["gather_floor"] = gather_floor(
             dm, (hi - lo + W - 1) // W * W * (8 if dtype == "f64" else 4), k1_ms,
             warm=lambda: plan.run(coeffs, 1, omega_kind=_lib.OMEGA_SPLITMIX, seed=7, col0=lo, d_global=d,
-                                 normalize_rows=(world == 1)))  # the same E the downstream legs read
+                                 normalize_rows=(world == 1)),  # the same E the downstream legs read
+            ncu_dtype=dtype if world == 1 else None)
         if traffic:
             # K1 against HBM on its ACTUAL traffic (ncu bytes per launch over the live K1
             # time): between the live random-row ceiling (its gathers' misses) and the
