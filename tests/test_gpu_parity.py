@@ -1326,3 +1326,66 @@ class TestValueFree:
             b = _device_result(plan, 80)
             assert bool((a == b).all())
             dm.close()
+
+
+def test_fuzz_split_exchange_bit_exact():
+    """Random CSR shapes through the split exchange (csemb_plan_partition_split)
+    with 1-4 emulated ranks: fp64 bit-identical to the split-order restatement
+    (strict stored order inside each part), within rounding of the 1-GPU order."""
+    import torch
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    from conftest import split_order_stage
+    from paper_1509_08360_b200.distributed import local_rows, row_blocks
+
+    @settings(max_examples=int(os.environ.get("CSEMB_FUZZ_EXAMPLES", "25")), deadline=None)
+    @given(n=st.integers(1, 300), density=st.floats(0.0, 0.2), d=st.integers(1, 40), L=st.integers(1, 7),
+           world=st.integers(1, 4), seed=st.integers(0, 2**31))
+    def check(n, density, d, L, world, seed):
+        rng = np.random.default_rng(seed)
+        a = rng.standard_normal((n, n)) * (rng.random((n, n)) < density)
+        a = 0.5 * (a + a.T)
+        nrm = np.linalg.norm(a, 2) if a.any() else 1.0
+        S = pb.SparseMatrix.from_dense(a / (1.05 * nrm))
+        th = rng.standard_normal(L + 1) * 0.5
+        om = O.sample_projection(n, d, seed % 1000)
+        n_pad, blocks = row_blocks(n, world)
+        ld = -(-d // 2) * 2
+        F = torch.zeros((world * n_pad, ld), dtype=torch.float64, device="cuda")
+        ranks = []
+        for lo, hi in blocks:
+            if hi <= lo:
+                continue
+            dm = pb.DeviceMatrix(local_rows(S, lo, hi), "float64")
+            plan = dm.plan(d)
+            plan.set_load_balance(split_threshold=0)
+            q = [torch.zeros((n_pad, ld), dtype=torch.float64, device="cuda") for _ in range(2)]
+            plan.partition_split(lo, n, F.data_ptr(), q[0].data_ptr(), q[1].data_ptr())
+            torch.cuda.synchronize()
+            plan.begin(th, omega_kind=1, seed=seed % 1000)
+            ranks.append((lo, hi, dm, plan, q))
+        for _, _, dm, _, _ in ranks:
+            dm.ctx.sync()
+        for r in range(1, L + 1):
+            for *_, plan, _ in ranks:
+                plan.step_local(r)
+            for *_, plan, _ in ranks:
+                plan.step(r)
+            for _, _, dm, _, _ in ranks:
+                dm.ctx.sync()
+            if r < L:
+                for lo, hi, dm, plan, q in ranks:
+                    F[lo:hi] = q[r & 1][:hi - lo]
+                torch.cuda.synchronize()
+        got = []
+        for lo, hi, dm, plan, q in ranks:
+            plan.end(False)
+            got.append(plan.download())
+            dm.close()
+        got = np.concatenate(got)
+        assert np.array_equal(got, split_order_stage(O.CSR.of(S), th, om, blocks))
+        ref, _, _ = O.run_stage(O.CSR.of(S), th, om)
+        assert rel(got, ref) <= 1e-12 or np.linalg.norm(ref) < 1e-300
+
+    check()
