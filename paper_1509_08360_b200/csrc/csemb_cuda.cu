@@ -372,8 +372,28 @@ static int64_t heavy_window_bytes() {
 
 // Build (or fetch) the schedule of matrix m for group width G; `row_bytes` is
 // the size of one gathered row of a column tile (sets the heavy-row window).
+static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out, int64_t row_bytes);
+#ifdef CSEMB_TRACE_SCHEDULE
+#include <chrono>
+#endif
 static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
                         int64_t row_bytes = 0) {
+#ifdef CSEMB_TRACE_SCHEDULE
+    const size_t before = m->schedules.size();
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = get_schedule_impl(m, G, threshold, order, out, row_bytes);
+    cudaStreamSynchronize(m->ctx->stream);
+    if (m->schedules.size() != before)
+        fprintf(stderr, "[schedule] built G=%d n=%lld in %.3f ms\n", G, (long long)m->n_rows,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    return rc;
+#else
+    return get_schedule_impl(m, G, threshold, order, out, row_bytes);
+#endif
+}
+
+static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
+                             int64_t row_bytes) {
     *out = nullptr;
     const int64_t wbytes = heavy_window_bytes();
     int64_t wcols = (wbytes > 0 && row_bytes > 0) ? std::max<int64_t>(1, wbytes / row_bytes) : 0;
