@@ -217,7 +217,56 @@ __global__ void k_split_fill(const int64_t *__restrict__ rowptr, const int *__re
     }
 }
 
+// schedule keys: (window index, min(exact ? len : ceil(len / G), cap)), ids = row
+__global__ void k_sched_keys(const int64_t *__restrict__ rowptr, int64_t n, int G, int exact, int64_t window,
+                             uint64_t *keys, int *ids) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = rowptr[i + 1] - rowptr[i];
+        const int64_t k = exact ? len : (len + G - 1) / G;
+        const uint64_t key = (uint64_t)(k < (1 << 16) ? k : (1 << 16));
+        const uint64_t w = window > 0 ? (uint64_t)(i / window) : 0ull;
+        keys[i] = (w << 17) | key;
+        ids[i] = (int)i;
+    }
+}
+
 }  // namespace
+
+int sched_order_device(csemb_mat *m, int G, bool exact, int64_t window, int **perm_out) {
+    csemb_ctx *c = m->ctx;
+    cudaStream_t s = c->stream;
+    const int64_t n = m->n_rows;
+    *perm_out = nullptr;
+    Scratch tmp(c);
+    uint64_t *keys = nullptr, *keys2 = nullptr;
+    int *ids = nullptr, *perm = nullptr;
+    CK(tmp.get(&keys, 8 * (size_t)n));
+    CK(tmp.get(&keys2, 8 * (size_t)n));
+    CK(tmp.get(&ids, 4 * (size_t)n));
+    CK(dmalloc(c, &perm, 4 * (size_t)n));
+    const int64_t nwin = window > 0 ? (n + window - 1) / window : 1;
+    int bits = 17;
+    while (bits < 64 && (nwin - 1) >> (bits - 17)) ++bits;
+    auto run = [&]() -> cudaError_t {
+        k_sched_keys<<<c->sm_count * 8, 256, 0, s>>>(m->rowptr, n, G, exact ? 1 : 0, window, keys, ids);
+        cudaError_t e = cudaGetLastError();
+        size_t tb = 0;
+        void *ts = nullptr;
+        if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, ids, perm, n, 0, bits, s);
+        if (e == cudaSuccess) e = tmp.get(&ts, tb);
+        // LSD radix sort: stable, so rows of equal (window, key) keep their order
+        if (e == cudaSuccess) e = cub::DeviceRadixSort::SortPairs(ts, tb, keys, keys2, ids, perm, n, 0, bits, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the scratch is released on return
+        return e;
+    };
+    const cudaError_t e = run();
+    if (e != cudaSuccess) {
+        dfree(c, perm);
+        CK(e);
+    }
+    *perm_out = perm;
+    return CSEMB_OK;
+}
 
 int mat_split_columns(csemb_mat *m, int64_t lo, int64_t hi, csemb_mat **loc_out, csemb_mat **rem_out) {
     csemb_ctx *c = m->ctx;

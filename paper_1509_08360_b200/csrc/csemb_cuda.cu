@@ -375,12 +375,14 @@ static int64_t heavy_window_bytes() {
 static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out, int64_t row_bytes);
 #ifdef CSEMB_TRACE_SCHEDULE
 #include <chrono>
+static std::chrono::steady_clock::time_point g_sched_t0;
 #endif
 static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
                         int64_t row_bytes = 0) {
 #ifdef CSEMB_TRACE_SCHEDULE
     const size_t before = m->schedules.size();
     const auto t0 = std::chrono::steady_clock::now();
+    g_sched_t0 = t0;
     const int rc = get_schedule_impl(m, G, threshold, order, out, row_bytes);
     cudaStreamSynchronize(m->ctx->stream);
     if (m->schedules.size() != before)
@@ -390,6 +392,25 @@ static int get_schedule(csemb_mat *m, int G, int64_t threshold, int order, Sched
 #else
     return get_schedule_impl(m, G, threshold, order, out, row_bytes);
 #endif
+}
+
+// Row-order window of a schedule (order 2 / auto on a moderate length spread):
+// a window of consecutive rows, not commensurate with the grid's rows per wave
+// (see the comment at the call site).  0: no windowing.
+static int64_t sched_window(const csemb_mat *m, int G, int order, bool skewed) {
+    int64_t window = order >= 64 ? order : 0;
+    if (order == 2 || (order < 0 && !skewed)) {
+        const int64_t wave = (int64_t)m->ctx->sm_count * 2 * 8 * (32 / G);  // 2 x 256-thread CTAs per SM
+        window = 8192;
+        for (int64_t w : {8192, 4096, 16384}) {
+            const double r = (double)(wave % w) / (double)w;
+            if (r > 0.1 && r < 0.9) {
+                window = w;
+                break;
+            }
+        }
+    }
+    return window;
 }
 
 static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
@@ -405,6 +426,53 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
         }
     const std::vector<int64_t> &rp = m->rowptr_host;
     const int64_t n = m->n_rows;
+    {
+        // Fast path, no row above the split threshold (config 2, every plain
+        // graph): the light rows are all rows, and their order -- the stable
+        // sort by (window, key) that the host counting sort below produces --
+        // is built on the device (sched_order_device, build.cu) instead of in
+        // host loops: ~5 ms -> ~1 ms per new config-2 matrix.  Same statistics
+        // in the same summation order, so the same mode and permutation.
+        int64_t maxlen = 0;
+        double s1 = 0.0, s2 = 0.0;
+        for (int64_t r = 0; r < n; ++r) {
+            const int64_t len = rp[r + 1] - rp[r];
+            maxlen = len > maxlen ? len : maxlen;
+            s1 += (double)len;
+            s2 += (double)len * (double)len;
+        }
+        static const bool host_only = getenv("CSEMB_SCHED_HOST") != nullptr;  // A/B: the host path below
+        if (!host_only && !(threshold > 0 && maxlen > threshold)) {
+            const double nl = (double)std::max<int64_t>(n, 1);
+            const double mean = s1 / nl, var = std::max(0.0, s2 / nl - mean * mean);
+            const bool skewed = mean > 0 && std::sqrt(var) > 0.5 * mean;
+            const int64_t window = sched_window(m, G, order, skewed);
+            const bool bucket = order == 1 || window > 0 || (order < 0 && skewed);
+            Schedule *sc = new Schedule();
+            sc->G = G;
+            sc->threshold = threshold;
+            sc->order = order;
+            sc->wcols = wcols;
+            sc->n_light = n;
+            if (bucket && n > 0) {
+                // window > 0: key = exact length for f64 matrices, else the batch count;
+                // global buckets: batch count (as the host path)
+                const bool exact = window > 0 && m->dtype == CSEMB_F64;
+#ifdef CSEMB_TRACE_SCHEDULE
+                fprintf(stderr, "[schedule] host stats done at %.3f ms\n", std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now() - g_sched_t0).count());
+#endif
+                const int rc = sched_order_device(m, G, exact, window, &sc->perm);
+                if (rc) {
+                    delete sc;
+                    return rc;
+                }
+            }
+            m->schedules.push_back(sc);
+            *out = sc;
+            return CSEMB_OK;
+        }
+    }
     std::vector<int> light, hrows, hoff(1, 0);
     std::vector<int64_t> cbeg, cend;
     light.reserve((size_t)n);
@@ -466,18 +534,7 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
     // the grid's rows per wave, or the warps whose grid-stride offsets keep landing
     // on the same window positions get all short (or all long) rows.
     const bool skewed = mean > 0 && std::sqrt(var) > 0.5 * mean;
-    int64_t window = order >= 64 ? order : 0;
-    if (order == 2 || (order < 0 && !skewed)) {
-        const int64_t wave = (int64_t)m->ctx->sm_count * 2 * 8 * (32 / G);  // 2 x 256-thread CTAs per SM
-        window = 8192;
-        for (int64_t w : {8192, 4096, 16384}) {
-            const double r = (double)(wave % w) / (double)w;
-            if (r > 0.1 && r < 0.9) {
-                window = w;
-                break;
-            }
-        }
-    }
+    const int64_t window = sched_window(m, G, order, skewed);
     const bool bucket = order == 1 || window > 0 || (order < 0 && skewed);
     if (window > 0) {  // stable counting sort by batch count inside each window
         const int64_t cap = 1 << 16;

@@ -103,4 +103,9 @@ CSEMB_INTERNAL void mat_free(csemb_mat *m);
 // rest (global ids); both keep each row's stored order (build.cu; call with
 // the context lock held)
 CSEMB_INTERNAL int mat_split_columns(csemb_mat *m, int64_t lo, int64_t hi, csemb_mat **loc, csemb_mat **rem);
+// the light-row order of a schedule with no split rows: rows 0..n-1 stably
+// sorted by (r / window, key), key = min(exact ? len : ceil(len / G), 2^16)
+// (window 0: one window); *perm is a new device array (dmalloc) of n ids
+// (build.cu; call with the context lock held)
+CSEMB_INTERNAL int sched_order_device(csemb_mat *m, int G, bool exact, int64_t window, int **perm);
 CSEMB_INTERNAL int grid_for(int64_t work_items, int threads, int sm_count, int per_sm = 8);
