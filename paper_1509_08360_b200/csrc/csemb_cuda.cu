@@ -433,13 +433,19 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
         // is built on the device (sched_order_device, build.cu) instead of in
         // host loops: ~5 ms -> ~1 ms per new config-2 matrix.  Same statistics
         // in the same summation order, so the same mode and permutation.
-        int64_t maxlen = 0;
-        double s1 = 0.0, s2 = 0.0;
-        for (int64_t r = 0; r < n; ++r) {
-            const int64_t len = rp[r + 1] - rp[r];
-            maxlen = len > maxlen ? len : maxlen;
-            s1 += (double)len;
-            s2 += (double)len * (double)len;
+        int64_t maxlen = m->len_max;
+        double s1 = m->len_s1, s2 = m->len_s2;
+        if (!m->len_stats) {
+            for (int64_t r = 0; r < n; ++r) {
+                const int64_t len = rp[r + 1] - rp[r];
+                maxlen = len > maxlen ? len : maxlen;
+                s1 += (double)len;
+                s2 += (double)len * (double)len;
+            }
+            m->len_max = maxlen;
+            m->len_s1 = s1;
+            m->len_s2 = s2;
+            m->len_stats = true;
         }
         static const bool host_only = getenv("CSEMB_SCHED_HOST") != nullptr;  // A/B: the host path below
         if (!host_only && !(threshold > 0 && maxlen > threshold)) {
@@ -853,13 +859,36 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
     *out = nullptr;
     CK(cudaSetDevice(c->device));
     if (n_rows < 0 || nnz < 0) return fail(CSEMB_ERR_INVALID, "negative matrix dimension");
-    int rc = check_offsets_host(row_offsets, n_rows, nnz);
-    if (rc) return rc;
+    if (row_offsets[0] != 0 || row_offsets[n_rows] != nnz)
+        return fail(CSEMB_ERR_INVALID, "row_offsets must run from 0 to nnz");
     csemb_mat *m = nullptr;
-    rc = mat_alloc(c, n_rows, n_cols, nnz, dtype, &m);
+    int rc = mat_alloc(c, n_rows, n_cols, nnz, dtype, &m);
     if (rc) return rc;
-    m->rowptr_host.assign(row_offsets, row_offsets + n_rows + 1);
     cudaStream_t s = c->stream;
+    // the host-side pass over the offsets (monotonicity, the host copy the
+    // schedule builder reads, row-length statistics) runs while the first
+    // chunk's copies are in flight: host_pass() is called right after they
+    // are enqueued
+    bool host_done = false;
+    auto host_pass = [&]() -> int {
+        host_done = true;
+        int r = check_offsets_host(row_offsets, n_rows, nnz);
+        if (r) return r;
+        m->rowptr_host.assign(row_offsets, row_offsets + n_rows + 1);
+        int64_t mx = 0;
+        double s1 = 0.0, s2 = 0.0;
+        for (int64_t i = 0; i < n_rows; ++i) {
+            const int64_t len = row_offsets[i + 1] - row_offsets[i];
+            mx = len > mx ? len : mx;
+            s1 += (double)len;
+            s2 += (double)len * (double)len;
+        }
+        m->len_max = mx;
+        m->len_s1 = s1;
+        m->len_s2 = s2;
+        m->len_stats = true;
+        return CSEMB_OK;
+    };
     cudaError_t e = cudaMemcpyAsync(m->rowptr, row_offsets, sizeof(int64_t) * (size_t)(n_rows + 1),
                                     cudaMemcpyHostToDevice, s);
     const int64_t CH = std::min<int64_t>(std::max<int64_t>(nnz, 1), (int64_t)1 << 25);
@@ -878,9 +907,14 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
             rc = mat_fill_chunk(m, off, cnt, st_cols, 8, (const double *)st_vals, bad);
             if (rc) break;
         }
+        if (e == cudaSuccess && !host_done) {
+            rc = host_pass();
+            if (rc) break;
+        }
         // the staging buffers are reused: finish this chunk before the next copy
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     }
+    if (e == cudaSuccess && !rc && !host_done) rc = host_pass();  // nnz == 0
     int hbad = 0;
     if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
@@ -888,6 +922,7 @@ extern "C" int csemb_matrix_upload(csemb_ctx *c, int64_t n_rows, int64_t n_cols,
     dfree(c, st_vals);
     dfree(c, bad);
     if (rc || e != cudaSuccess) {
+        cudaStreamSynchronize(s);  // copies from the caller's arrays may still be in flight
         mat_free(m);
         if (rc) return rc;
         cudaGetLastError();

@@ -90,6 +90,12 @@ struct csemb_mat {
     // checked once, lazily, on the context stream (-1 = not checked yet)
     int *vf_flag = nullptr;
     int vf_state = -1;
+    // row-length statistics (max, sum, sum of squares in row order), computed on
+    // the host while csemb_matrix_upload's copies are in flight; the schedule
+    // builder reuses them
+    bool len_stats = false;
+    int64_t len_max = 0;
+    double len_s1 = 0.0, len_s2 = 0.0;
 };
 
 CSEMB_INTERNAL size_t dsize(int dtype);
