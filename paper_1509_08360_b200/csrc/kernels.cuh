@@ -261,6 +261,10 @@ __device__ __forceinline__ bool vfinite(float4 q) {
 #define GATHER_OP "ld.global.nc.L1::no_allocate"
 #elif GATHER_MODE == 2
 #define GATHER_OP "ld.global.cg"
+#elif GATHER_MODE == 3
+#define GATHER_OP "ld.global.nc.L2::256B"  // 256-byte L2 fills for gathered rows (experiment)
+#elif GATHER_MODE == 4
+#define GATHER_OP "ld.global.nc.L2::128B"
 #else
 #define GATHER_OP "ld.global.nc"
 #endif
