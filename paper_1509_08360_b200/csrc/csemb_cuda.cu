@@ -133,13 +133,19 @@ static std::mutex g_occ_mu;
 static std::unordered_map<const void *, int> g_occ;
 
 // Staged K1 variants for groups of >= 8 lanes (CSEMB_K1_TMA): 1 = TMA bulk copies
-// into per-warp mbarrier rings, 2 = per-lane cp.async rings; 0 (default) = registers.
-static int use_tma() {
+// into per-warp mbarrier rings, 2 = per-lane cp.async rings (both stage the GATHERED
+// rows; measured 2x slower), 3 = register gathers with the column-index / value
+// batches staged in a warp-private shared-memory double buffer (cp.async in, one
+// broadcast LDS per entry out, instead of register batches + shuffles), 0 = register
+// batches.  Unset: 3 for fp32 (measured, round 2 session 4: config 3 11.04 -> 10.73 ms,
+// config 4 11.87 -> 11.57 ms per step, config 2 unchanged within noise), 0 for fp64
+// (config 2 d=80: 1.178 -> 1.198 ms with staging).
+static int use_tma(bool is_f32) {
     static int on = [] {
         const char *e = getenv("CSEMB_K1_TMA");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : -1;
     }();
-    return on;
+    return on >= 0 ? on : (is_f32 ? 3 : 0);
 }
 
 template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED, int PEERS = 0>
@@ -157,6 +163,8 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
         P.smem_base = (int)((smem + 127) / 128 * 128);
         if (STAGED == 1)
             smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
+        else if (STAGED == 3)  // two batch slots per warp, at most 64 entries (ids + values) each
+            smem = P.smem_base + (size_t)(threads / 32) * 2 * 64 * (4 + sizeof(T));
         else
             smem = P.smem_base + (size_t)S * threads * VPL * 16;
         max_smem = smem;
@@ -188,14 +196,16 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
 
 template <typename T, int G, int VPL, int MODE, int PEAK>
 static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
-    if constexpr (G >= 8) {
-        if (use_tma() == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
-        if (use_tma() == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
-    }
     // fused row-partition exchange: peer stores in the epilogue (PEAK_FLAG steps)
     if constexpr (MODE == MODE_RECUR && PEAK == PEAK_FLAG) {
         if (P.mc) return run_step_t<T, G, VPL, MODE, PEAK, 0, 2>(P, s, sm_count);
         if (P.n_peer) return run_step_t<T, G, VPL, MODE, PEAK, 0, 1>(P, s, sm_count);
+    }
+    if constexpr (G >= 8) {
+        const int staged = use_tma(sizeof(T) == 4);
+        if (staged == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
+        if (staged == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
+        if (staged == 3 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 3>(P, s, sm_count);
     }
     return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
 }

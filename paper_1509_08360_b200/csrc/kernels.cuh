@@ -344,6 +344,24 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
                  : "memory");
 }
+// per-lane 4- / 8-byte async copies (index / value staging, STAGED == 3)
+#ifndef K1_SIDX_HINT
+#define K1_SIDX_HINT 0  // 1: L2 evict-first policy on the staged index / value copies (experiment)
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void *smem, const void *gmem, uint64_t pol) {
+#if K1_SIDX_HINT
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], %2, %3;" ::"r"(smem_u32(smem)), "l"(gmem), "n"(BYTES), "l"(pol)
+                 : "memory");
+#else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(smem)), "l"(gmem), "n"(BYTES) : "memory");
+#endif
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -450,7 +468,6 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     auto bcast_a = [&](const T (&a)[EB], int t) { return __shfl_sync(0xFFFFFFFFu, a[t / G], t % G, G); };
     int myj[EB];
     T mya[EB];
-    load_batch(beg, end, end - beg, myj, mya);
 
     // Gathers of the first D-1 entries of the current batch are carried across
     // batches.  Register variant: D-deep rotating register buffer.  Staged
@@ -463,15 +480,66 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                                               : (sizeof(T) == 8 ? ((G == 4 || (G == 32 && MODE == MODE_SPMM) || PEAK == PEAK_EXACT)
                                                                        ? K1_DEPTH_F64_SPILLY : 4)
                                                                 : K1_DEPTH_F32));
-    constexpr int D = STAGED ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
+    // RING: the gathered rows go through shared memory (STAGED 1 / 2); SIDX
+    // (STAGED 3): the gathers stay in registers and the column-index / value
+    // batches are staged in a warp-private shared-memory double buffer instead
+    constexpr bool RING = STAGED == 1 || STAGED == 2;
+    constexpr bool SIDX = STAGED == 3;
+    constexpr int D = RING ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
     // STAGED == 2: per-lane ring of D entries x VPL 16-byte slots in shared memory
     VT *lring = nullptr;
     if constexpr (STAGED == 2)
         lring = reinterpret_cast<VT *>(k1_dyn_smem + P.smem_base) + (size_t)threadIdx.x * VPL;
     static_assert(B % D == 0, "pipeline depth must divide the batch width");
-    VT buf[STAGED ? 1 : D][VPL];
+    // SIDX: warp-private double buffer of entry batches in shared memory, slot =
+    // [RPW][B] column ids then [RPW][B] values.  Lane t % G of a group copies
+    // entry t of its row's batch with a 4- / 8-byte cp.async (padding entries are
+    // stored as zeros); every lane of the group then reads entry t back with one
+    // broadcast LDS instead of a shuffle.  `scur` (warp-uniform) is the slot of
+    // the current batch, scur ^ 1 receives the next one while this one is consumed.
+    constexpr int SLOT_BYTES = RPW * B * (4 + (int)sizeof(T));
+    unsigned char *sidx = nullptr;
+    if constexpr (SIDX) sidx = k1_dyn_smem + P.smem_base + (size_t)(threadIdx.x >> 5) * 2 * SLOT_BYTES;
+    int scur = 0;
+    const uint64_t sidx_pol = (SIDX && K1_SIDX_HINT) ? l2_evict_first_policy() : 0ull;
+    auto slot_j = [&](int slot) { return reinterpret_cast<int *>(sidx + slot * SLOT_BYTES) + grp * B; };
+    auto slot_a = [&](int slot) { return reinterpret_cast<T *>(sidx + slot * SLOT_BYTES + RPW * B * 4) + grp * B; };
+    auto stage_batch = [&](int64_t b0, int64_t e0, int slot) {
+        __syncwarp();  // the slot's previous contents have been read by every lane
+        int *dj = slot_j(slot);
+        T *da = slot_a(slot);
 #pragma unroll
-    for (int i = 0; i < (STAGED ? 1 : D); ++i)
+        for (int k = 0; k < EB; ++k) {
+            const int t = gl + k * G;
+            const int64_t q = b0 + t;
+            if (gl < BL) {
+                if (q < e0) {
+                    cp_async_small<4>(dj + t, cols + q, sidx_pol);
+                    cp_async_small<(int)sizeof(T)>(da + t, vals + q, sidx_pol);
+                } else {
+                    dj[t] = 0;
+                    da[t] = (T)0;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    auto stage_wait = [&]() {  // the staged batch is visible to the whole warp
+        cp_async_wait<0>();
+        __syncwarp();
+    };
+    auto sjr = [&](int slot, int t) { return *reinterpret_cast<volatile int *>(slot_j(slot) + t); };
+    auto sar = [&](int slot, int t) { return *reinterpret_cast<volatile T *>(slot_a(slot) + t); };
+    if constexpr (SIDX) {
+        static_assert(!K1_TRIM, "index staging has no trimmed-batch path");
+        stage_batch(beg, end, 0);
+        stage_wait();
+    } else {
+        load_batch(beg, end, end - beg, myj, mya);
+    }
+    VT buf[RING ? 1 : D][VPL];
+#pragma unroll
+    for (int i = 0; i < (RING ? 1 : D); ++i)
 #pragma unroll
         for (int k = 0; k < VPL; ++k) buf[i][k] = vzero(VT());
     uint64_t *bars = nullptr;
@@ -519,7 +587,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         }
     };
 #pragma unroll
-    for (int e = 0; e < D - 1; ++e) issue(e, bcast_j(myj, e), e < end - beg);
+    for (int e = 0; e < D - 1; ++e) issue(e, SIDX ? sjr(0, e) : bcast_j(myj, e), e < end - beg);
 
     for (int64_t wbase = warp * RPW; wbase < P.n_rows; wbase += wstride) {  // warp-uniform
         const bool active = it < P.n_rows;
@@ -566,7 +634,19 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             int nj[EB];
             T na[EB];
             int ncnt = 0;  // entries of that next batch for my row
-            if (b + 1 < nb_mine) {
+            if constexpr (SIDX) {
+                int64_t nb0 = 0, ne0 = 0;  // empty range: a batch of zeros
+                if (b + 1 < nb_mine) {
+                    ncnt = len - (b + 1) * B;
+                    nb0 = beg + (b + 1) * B;
+                    ne0 = end;
+                } else if (b + 1 >= nb) {
+                    ncnt = (int)(end2 - beg2);
+                    nb0 = beg2;
+                    ne0 = end2;
+                }
+                stage_batch(nb0, ne0, scur ^ 1);
+            } else if (b + 1 < nb_mine) {
                 ncnt = len - (b + 1) * B;
                 load_batch(beg + (b + 1) * B, end, end - beg, nj, na);
             } else if (b + 1 >= nb) {
@@ -604,7 +684,12 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                 const int e = t + D - 1;
                 int j;
                 bool more;
-                if constexpr (FULL) {
+                if constexpr (SIDX) {
+                    // the next batch is first read at step B - D + 1 (entry e = B)
+                    if (D > 1 && t == B - D + 1) stage_wait();
+                    j = sjr(e < B ? scur : scur ^ 1, e % B);
+                    more = (e < B) ? (e < cnt) : (e - B < ncnt);
+                } else if constexpr (FULL) {
                     j = (e < B) ? bcast_j(myj, e % B) : bcast_j(nj, e % B);
                     more = (e < B) ? (e < cnt) : (e - B < ncnt);
                 } else {
@@ -614,7 +699,11 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                     more = cur ? (e < cnt) : (e - ns < ncnt);
                 }
                 if (D > 1) issue(e % D, j, more);
-                const T a = bcast_a(mya, t);
+                T a;
+                if constexpr (SIDX)
+                    a = sar(scur, t);
+                else
+                    a = bcast_a(mya, t);
                 if (D == 1) issue(0, j, more);
                 if constexpr (STAGED == 2) {
                     cp_async_wait<D - 1>();  // entry t has landed (this lane's own copies)
@@ -652,7 +741,10 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
                     step(t, nst, std::false_type{});
                 }
             }
-            if (b + 1 < nb_mine || b + 1 >= nb) {
+            if constexpr (SIDX) {
+                if (D == 1) stage_wait();
+                scur ^= 1;
+            } else if (b + 1 < nb_mine || b + 1 >= nb) {
 #pragma unroll
                 for (int k = 0; k < EB; ++k) {
                     myj[k] = nj[k];
@@ -661,9 +753,14 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             }
         }
         if (nb == 0) {  // every row of the warp is empty: move to the next rows' first batch
-            load_batch(beg2, end2, end2 - beg2, myj, mya);
+            if constexpr (SIDX) {
+                stage_batch(beg2, end2, scur);
+                stage_wait();
+            } else {
+                load_batch(beg2, end2, end2 - beg2, myj, mya);
+            }
 #pragma unroll
-            for (int e = 0; e < D - 1; ++e) issue(e, bcast_j(myj, e), e < end2 - beg2);
+            for (int e = 0; e < D - 1; ++e) issue(e, SIDX ? sjr(scur, e) : bcast_j(myj, e), e < end2 - beg2);
         }
 
         if (active) {
@@ -732,7 +829,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         end = end2;
     }
 
-    if constexpr (STAGED == 2) cp_async_wait<0>();
+    if constexpr (STAGED == 2 || STAGED == 3) cp_async_wait<0>();
     if constexpr (PEERS == 2) asm volatile("fence.proxy.alias;" ::: "memory");  // multicast vs unicast aliases
     if constexpr (PEERS) __threadfence_system();  // peer stores performed before the step's barrier
     if (MODE == MODE_RECUR && P.peaks) {
