@@ -380,6 +380,30 @@ static int64_t heavy_window_bytes() {
     return b;
 }
 
+// Hot heavy rows (CSEMB_HOT_ROWS = H, CSEMB_HOT_WINDOW = W columns): the H
+// longest heavy rows -- those with at least 16 entries per W-column window on
+// average -- are cut at every multiple of W columns instead of into fixed
+// chunks, and their pieces are swept window by window, rows in length order
+// inside a window.  The 32 pieces a CTA works on at a time (8 warps x 32/G
+// rows) then gather from the SAME W rows of Q(r-1) (W x row bytes <= ~100 KB),
+// so all but the first touch of a gathered row are L1 hits instead of L2 -> SM
+// transfers: config 4's most frequent terms appear in most documents, and
+// every one of their entries otherwise crosses the crossbar on its own.
+static int hot_rows_opt() {
+    static int v = [] {
+        const char *e = getenv("CSEMB_HOT_ROWS");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+static int64_t hot_window_opt() {
+    static int64_t v = [] {
+        const char *e = getenv("CSEMB_HOT_WINDOW");
+        return (int64_t)(e ? atoll(e) : 256);
+    }();
+    return v;
+}
+
 // Build (or fetch) the schedule of matrix m for group width G; `row_bytes` is
 // the size of one gathered row of a column tile (sets the heavy-row window).
 static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out, int64_t row_bytes);
@@ -491,6 +515,7 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
     }
     std::vector<int> light, hrows, hoff(1, 0);
     std::vector<int64_t> cbeg, cend;
+    std::vector<int> cwin;  // column window of each chunk (windowed schedules)
     light.reserve((size_t)n);
     double sum = 0.0, sum2 = 0.0;
     for (int64_t r = 0; r < n; ++r) {
@@ -529,11 +554,82 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
             return fail(CSEMB_ERR_CUDA, "schedule window bounds: %s", cudaGetErrorString(e));
         }
     }
+    // hot heavy rows: rank (by descending length) of heavy row h, or -1
+    std::vector<int> hot_rank(hrows.size(), -1);
+    std::vector<int64_t> hbounds;  // [hot rank][nwh + 1] window boundaries
+    const int64_t hotw = hot_window_opt();
+    const int nwh = hotw > 0 ? (int)((m->n_cols + hotw - 1) / hotw) : 0;
+    if (hot_rows_opt() > 0 && hotw > 0 && wcols == 0 && !hrows.empty()) {
+        std::vector<int> cand;
+        for (size_t h = 0; h < hrows.size(); ++h)
+            if (rp[hrows[h] + 1] - rp[hrows[h]] >= (int64_t)nwh * 16) cand.push_back((int)h);
+        std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+            return rp[hrows[a] + 1] - rp[hrows[a]] > rp[hrows[b] + 1] - rp[hrows[b]];
+        });
+        if ((int)cand.size() > hot_rows_opt()) cand.resize((size_t)hot_rows_opt());
+        if (!cand.empty()) {
+            std::vector<int> rows(cand.size());
+            for (size_t i = 0; i < cand.size(); ++i) {
+                hot_rank[(size_t)cand[i]] = (int)i;
+                rows[i] = hrows[(size_t)cand[i]];
+            }
+            int *drows = nullptr;
+            int64_t *dbounds = nullptr;
+            const size_t nb = rows.size() * (size_t)(nwh + 1);
+            cudaError_t e = dmalloc(m->ctx, &drows, 4 * rows.size());
+            if (e == cudaSuccess) e = dmalloc(m->ctx, &dbounds, 8 * nb);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(drows, rows.data(), 4 * rows.size(), cudaMemcpyHostToDevice, m->ctx->stream);
+            if (e == cudaSuccess) {
+                k_window_bounds<<<grid_for((int64_t)nb, 256, m->ctx->sm_count, 8), 256, 0, m->ctx->stream>>>(
+                    m->cols, m->rowptr, drows, (int)rows.size(), nwh, hotw, dbounds);
+                e = cudaGetLastError();
+            }
+            hbounds.resize(nb);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(hbounds.data(), dbounds, 8 * nb, cudaMemcpyDeviceToHost, m->ctx->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(m->ctx->stream);
+            dfree(m->ctx, drows);
+            dfree(m->ctx, dbounds);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(CSEMB_ERR_CUDA, "schedule hot-row bounds: %s", cudaGetErrorString(e));
+            }
+        }
+    }
+    std::vector<int64_t> chot;  // per chunk: window * 2^20 + rank of a hot piece, -1 otherwise
     for (size_t h = 0; h < hrows.size(); ++h) {
         const int r = hrows[h];
+        if (hot_rank[h] >= 0) {
+            const int64_t *bw = hbounds.data() + (size_t)hot_rank[h] * (size_t)(nwh + 1);
+            for (int k = 0; k < nwh; ++k) {
+                // the last boundary is the row end (k_window_bounds searches col >= nwh * W: none)
+                for (int64_t b = bw[k]; b < bw[k + 1]; b += HEAVY_CHUNK) {
+                    cbeg.push_back(b);
+                    cend.push_back(std::min(b + HEAVY_CHUNK, bw[k + 1]));
+                    chot.resize(cbeg.size(), -1);
+                    chot.back() = ((int64_t)k << 20) + hot_rank[h];
+                }
+            }
+            hoff.push_back((int)cbeg.size());
+            continue;
+        }
         for (int k = 0; k < nwin; ++k) {
             const int64_t s0 = wcols > 0 ? bounds[h * (nwin + 1) + k] : rp[r];
             const int64_t s1 = wcols > 0 ? bounds[h * (nwin + 1) + k + 1] : rp[r + 1];
+            if (wcols > 0) {
+                // a window segment is cut into equal pieces (<= HEAVY_CHUNK, multiples of
+                // 8 entries), so the chunks of one window have few distinct lengths
+                const int64_t seg = s1 - s0;
+                if (seg <= 0) continue;
+                const int64_t np = (seg + HEAVY_CHUNK - 1) / HEAVY_CHUNK;
+                const int64_t piece = (((seg + np - 1) / np) + 7) & ~(int64_t)7;
+                for (int64_t b = s0; b < s1; b += piece) {
+                    cbeg.push_back(b);
+                    cend.push_back(std::min(b + piece, s1));
+                    cwin.push_back(k);
+                }
+                continue;
+            }
             for (int64_t b = s0; b < s1; b += HEAVY_CHUNK) {
                 cbeg.push_back(b);
                 cend.push_back(std::min(b + HEAVY_CHUNK, s1));
@@ -626,7 +722,28 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
         if (e == cudaSuccess) {
             std::vector<int> ord(cbeg.size());
             for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
-            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hfirst[a] < hfirst[b]; });
+            chot.resize(cbeg.size(), -1);
+            bool any_hot = false;
+            for (int64_t v : chot) any_hot |= v >= 0;
+            if (any_hot) {
+                // hot pieces first, window by window and by row rank inside a window; then
+                // the other chunks by first column
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+                    const bool ha = chot[a] >= 0, hb = chot[b] >= 0;
+                    if (ha != hb) return ha;
+                    return ha ? chot[a] < chot[b] : hfirst[a] < hfirst[b];
+                });
+            } else if (!cwin.empty()) {
+                // windowed: window by window (the window's gathered rows stay in L2), and
+                // inside a window by descending batch count, so the chunks a warp takes
+                // together have the same length (the batch loop is warp-uniform)
+                auto nbat = [&](int c) { return (cend[c] - cbeg[c] + G - 1) / G; };
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+                    return cwin[a] != cwin[b] ? cwin[a] < cwin[b] : nbat(a) > nbat(b);
+                });
+            } else {
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return hfirst[a] < hfirst[b]; });
+            }
             e = dmalloc(m->ctx, &sc->corder, 4 * ord.size());
             if (e == cudaSuccess) e = cudaMemcpyAsync(sc->corder, ord.data(), 4 * ord.size(), cudaMemcpyHostToDevice, m->ctx->stream);
         }

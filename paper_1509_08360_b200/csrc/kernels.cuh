@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             constexpr bool TRIM = K1_TRIM && STAGED == 0 && D - 1 <= G;
             const int nst = (TRIM && b + 1 == nb) ? min(B, (smax - b * B + D - 1) / D * D) : B;
             auto step = [&](const int t, const int ns, auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
+                [[maybe_unused]] constexpr bool FULL = decltype(full_tag)::value;
 #if K1_GATHER_PF
                 // L2 prefetch of entry t of the NEXT batch (B steps ahead, no registers):
                 // lanes gl < pf_lines each request one 128-byte line of that row, so the
