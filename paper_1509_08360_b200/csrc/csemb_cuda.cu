@@ -163,7 +163,7 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
         P.smem_base = (int)((smem + 127) / 128 * 128);
         if (STAGED == 1)
             smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
-        else if (STAGED == 3)  // two batch slots per warp, at most 64 entries (ids + values) each
+        else if (STAGED == 3 || STAGED == 4)  // two batch slots per warp, at most 64 entries (ids + values) each
             smem = P.smem_base + (size_t)(threads / 32) * 2 * 64 * (4 + sizeof(T));
         else
             smem = P.smem_base + (size_t)S * threads * VPL * 16;
@@ -206,6 +206,7 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
         if (staged == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
         if (staged == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
         if (staged == 3 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 3>(P, s, sm_count);
+        if (staged == 4 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 4>(P, s, sm_count);
     }
     return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
 }

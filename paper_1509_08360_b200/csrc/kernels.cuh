@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     // (STAGED 3): the gathers stay in registers and the column-index / value
     // batches are staged in a warp-private shared-memory double buffer instead
     constexpr bool RING = STAGED == 1 || STAGED == 2;
-    constexpr bool SIDX = STAGED == 3;
+    constexpr bool SIDX = STAGED == 3 || STAGED == 4;
+    constexpr bool SREG = STAGED == 4;  // the batch travels LDG.cs -> registers -> STS instead of cp.async
     constexpr int D = RING ? ((K1T_STAGES < B) ? K1T_STAGES : B) : ((DEPTH < B) ? DEPTH : B);
     // STAGED == 2: per-lane ring of D entries x VPL 16-byte slots in shared memory
     VT *lring = nullptr;
@@ -504,7 +505,24 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
     const uint64_t sidx_pol = (SIDX && K1_SIDX_HINT) ? l2_evict_first_policy() : 0ull;
     auto slot_j = [&](int slot) { return reinterpret_cast<int *>(sidx + slot * SLOT_BYTES) + grp * B; };
     auto slot_a = [&](int slot) { return reinterpret_cast<T *>(sidx + slot * SLOT_BYTES + RPW * B * 4) + grp * B; };
+    int pj[EB];  // SREG: the batch in flight (registers) and its slot
+    T pa[EB];
+    int pslot = 0;
     auto stage_batch = [&](int64_t b0, int64_t e0, int slot) {
+        if constexpr (SREG) {
+            pslot = slot;
+#pragma unroll
+            for (int k = 0; k < EB; ++k) {
+                const int64_t q = b0 + gl + k * G;
+                pj[k] = 0;
+                pa[k] = (T)0;
+                if (gl < BL && q < e0) {
+                    pj[k] = __ldcs(cols + q);
+                    pa[k] = __ldcs(vals + q);
+                }
+            }
+            return;
+        }
         __syncwarp();  // the slot's previous contents have been read by every lane
         int *dj = slot_j(slot);
         T *da = slot_a(slot);
@@ -525,6 +543,19 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
         cp_async_commit();
     };
     auto stage_wait = [&]() {  // the staged batch is visible to the whole warp
+        if constexpr (SREG) {
+            __syncwarp();  // the slot's previous contents have been read by every lane
+            int *dj = slot_j(pslot);
+            T *da = slot_a(pslot);
+#pragma unroll
+            for (int k = 0; k < EB; ++k)
+                if (gl < BL) {
+                    dj[gl + k * G] = pj[k];
+                    da[gl + k * G] = pa[k];
+                }
+            __syncwarp();
+            return;
+        }
         cp_async_wait<0>();
         __syncwarp();
     };
