@@ -140,12 +140,17 @@ static std::unordered_map<const void *, int> g_occ;
 // batches.  Unset: 3 for fp32 (measured, round 2 session 4: config 3 11.04 -> 10.73 ms,
 // config 4 11.87 -> 11.57 ms per step, config 2 unchanged within noise), 0 for fp64
 // (config 2 d=80: 1.178 -> 1.198 ms with staging).
-static int use_tma(bool is_f32) {
+// Small sweeps (at most 4 waves of the grid: config 1) are bound by each warp's
+// dependent chain, where the staged copy's wait costs more than the shuffle's
+// (config 1 fp32: 0.556 -> 0.591 ms per embedding with staging), so they keep
+// the register batches.
+static int use_tma(bool is_f32, int64_t work_threads = INT64_MAX, int sm_count = 1) {
     static int on = [] {
         const char *e = getenv("CSEMB_K1_TMA");
         return e ? atoi(e) : -1;
     }();
-    return on >= 0 ? on : (is_f32 ? 3 : 0);
+    if (on >= 0) return on;
+    return (is_f32 && work_threads > (int64_t)4 * sm_count * 512) ? 3 : 0;
 }
 
 template <typename T, int G, int VPL, int MODE, int PEAK, int STAGED, int PEERS = 0>
@@ -163,8 +168,8 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
         P.smem_base = (int)((smem + 127) / 128 * 128);
         if (STAGED == 1)
             smem = P.smem_base + (size_t)(threads / 32) * (128 + (size_t)S * RPW * P.nvt * 16);
-        else if (STAGED == 3 || STAGED == 4)  // two batch slots per warp, at most 64 entries (ids + values) each
-            smem = P.smem_base + (size_t)(threads / 32) * 2 * 64 * (4 + sizeof(T));
+        else if (STAGED == 3 || STAGED == 4)  // two batch slots per warp of 32 * EB entries (ids + values) each
+            smem = P.smem_base + (size_t)(threads / 32) * 2 * (G >= 4 ? 64 : (G == 2 ? 128 : 256)) * (4 + sizeof(T));
         else
             smem = P.smem_base + (size_t)S * threads * VPL * 16;
         max_smem = smem;
@@ -202,12 +207,24 @@ static cudaError_t run_step(const StepParams &P, cudaStream_t s, int sm_count) {
         if (P.n_peer) return run_step_t<T, G, VPL, MODE, PEAK, 0, 1>(P, s, sm_count);
     }
     if constexpr (G >= 8) {
-        const int staged = use_tma(sizeof(T) == 4);
+        const int staged = use_tma(sizeof(T) == 4, P.n_rows * G, sm_count);
         if (staged == 1) return run_step_t<T, G, VPL, MODE, PEAK, 1>(P, s, sm_count);
         if (staged == 2) return run_step_t<T, G, VPL, MODE, PEAK, 2>(P, s, sm_count);
         if (staged == 3 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 3>(P, s, sm_count);
         if (staged == 4 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 4>(P, s, sm_count);
     }
+    // 4-lane groups (fp32 d = 33..48, e.g. config 1 and 2-GPU column shards of config 2):
+    // staged batches measured 0.445 -> 0.420 ms per step at d = 40; narrower groups lose
+    // 10-14% with it (two 1.5-3 KB slots per warp), fp64 4-lane groups gain nothing
+    if constexpr (G == 4 && sizeof(T) == 4) {
+        if (use_tma(true, P.n_rows * G, sm_count) == 3 && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 3>(P, s, sm_count);
+    }
+#ifdef K1_STAGE_NARROW  // experiment: staged entry batches for every narrow group
+    if constexpr (G < 8) {
+        static const bool narrow = getenv("CSEMB_K1_STAGE_NARROW") != nullptr;
+        if (narrow && !(K1_VF && P.vf)) return run_step_t<T, G, VPL, MODE, PEAK, 3>(P, s, sm_count);
+    }
+#endif
     return run_step_t<T, G, VPL, MODE, PEAK, 0>(P, s, sm_count);
 }
 
