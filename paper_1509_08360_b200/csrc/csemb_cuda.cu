@@ -476,22 +476,31 @@ static int64_t sched_window(const csemb_mat *m, int G, int order, bool skewed) {
 static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, Schedule **out,
                              int64_t row_bytes) {
     *out = nullptr;
-    // Column windows (session 4).  Automatic: 64 MB of gathered rows per window
-    // when the gathered block is at least 4 windows (else L2 already holds a good
-    // part of it).  Rows with at least 20 entries per window on average (but no
-    // more than CSEMB_HEAVY_WINDOW_MAXLEN = 65536: the hottest rows' fixed chunks
-    // already share their gathered rows in L2) are cut at the window boundaries
-    // and swept window by window, so the rows they gather are fetched from DRAM
-    // about once per step: config 4's moderately frequent terms (256..65536
-    // documents each, spread over 768 MB of document rows) go from all-miss
-    // gathers to L2 hits -- K1 10.64 -> 10.11 ms per step (short runs), config 3
-    // unchanged.  The caller's threshold of 0 (strict stored order) still
-    // disables every split.
-    int64_t wbytes = heavy_window_bytes();
-    const bool auto_window = wbytes < 0;
-    if (auto_window) wbytes = (int64_t)64 << 20;
-    int64_t wcols = (wbytes > 0 && row_bytes > 0) ? std::max<int64_t>(1, wbytes / row_bytes) : 0;
-    if (auto_window && wcols * 4 > m->n_cols) wcols = 0;
+    // Column windows (session 4).  Automatic: windows of 3 * 2^16 (fp32) / 2^16 (fp64)
+    // columns -- 50-75 MB of gathered rows at d = 80..96; measured sweep in
+    // profiles/r2_k1_experiments.txt -- on matrices with at
+    // least 8 of them.  Rows with at least 20 entries per window on average (but
+    // no more than CSEMB_HEAVY_WINDOW_MAXLEN = 65536: the hottest rows' fixed
+    // chunks already share their gathered rows in L2) are cut at the window
+    // boundaries and swept window by window, so the rows they gather are fetched
+    // from DRAM about once per step: config 4's moderately frequent terms
+    // (hundreds to 65536 documents each, spread over 768 MB of document rows) go
+    // from all-miss gathers to L2 hits.  The rule depends on the matrix and the
+    // dtype only -- not on the block width -- so every column shard cuts the same
+    // rows at the same entries and the result stays bit-identical for any GPU
+    // count.  The caller's threshold of 0 (strict stored order)
+    // still disables every split; CSEMB_HEAVY_WINDOW_MB (experiments) sets the
+    // window in bytes of the gathered block instead, 0 = no windows.
+    int64_t wcols = 0;
+    const int64_t wbytes = heavy_window_bytes();
+    if (wbytes < 0) {
+        static const int64_t w32 = getenv("CSEMB_WINDOW_COLS_F32") ? atoll(getenv("CSEMB_WINDOW_COLS_F32")) : ((int64_t)3 << 16);
+        static const int64_t w64 = getenv("CSEMB_WINDOW_COLS_F64") ? atoll(getenv("CSEMB_WINDOW_COLS_F64")) : ((int64_t)1 << 16);
+        wcols = m->dtype == CSEMB_F32 ? w32 : w64;
+        if (m->n_cols < 8 * wcols) wcols = 0;
+    } else if (wbytes > 0 && row_bytes > 0) {
+        wcols = std::max<int64_t>(1, wbytes / row_bytes);
+    }
     if (wcols >= m->n_cols) wcols = 0;  // one window: plain fixed chunks
     if (threshold <= 0) wcols = 0;
     if (wcols > 0) {

@@ -196,3 +196,33 @@ def test_config5_slice_row_partition_vs_oracle(dtype):
         c32 = cos_err(got, ref, n, 7)
         print(f"config 5 slice n={n} fp32: rel {r32:.3e}, cosine error {c32:.3e}")
         assert r32 <= FP32_REL and c32 <= COS_TOL, (r32, c32)
+
+
+def test_column_shards_bit_identical_with_windowed_heavy_rows():
+    """GPU-count invariance on a matrix where the automatic column
+    windows are active: 1.7e6 columns (>= 8 windows in both dtypes), hub rows
+    from 500 to 200 000 entries -- some under the plain 2048 split threshold
+    but over the windowed one, some windowed, some above the window length cap
+    (fixed chunks).  The cuts depend on the matrix and the dtype only, so three
+    column shards give the same bits as one block; fp64 also meets the oracle
+    gate (split rows change the summation order of those rows only)."""
+    n = 1_700_000
+    rng = np.random.default_rng(23)
+    hubs = [(7, 500), (1000, 1500), (50_000, 3000), (300_000, 20_000), (700_000, 66_000), (1_650_000, 200_000)]
+    parts = [rng.integers(0, n, size=(3_000_000, 2))]
+    for h, deg in hubs:
+        parts.append(np.stack([np.full(deg, h, np.int64), rng.choice(n, size=deg, replace=False)], 1))
+    S = pb.normalized_adjacency(np.concatenate(parts), n)
+    lens = np.diff(S.row_offsets)
+    assert lens.max() > 65536 and n >= 8 * (3 << 16)
+    th = pb.legendre_coefficients(pb.indicator_above(0.5), 6)
+    om = O.sample_projection(n, 24, 5)
+    ref, _, bad = O.run_stage(O.CSR.of(S), th.coeffs, om)
+    assert bad == 0
+    one64 = pb.fast_embed_eig(S, th, 6, om).values
+    assert rel(one64, ref) <= FP64_REL
+    assert not np.array_equal(one64, ref)  # the split path ran (hub rows are summed in pieces)
+    assert np.array_equal(pb.fast_embed_eig(S, th, 6, om, device=[0, 0, 0]).values, one64)
+    one32 = pb.fast_embed_eig(S, th, 6, om, dtype="float32").values
+    assert rel(one32, ref) <= FP32_REL
+    assert np.array_equal(pb.fast_embed_eig(S, th, 6, om, dtype="float32", device=[0, 0, 0]).values, one32)
