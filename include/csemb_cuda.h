@@ -151,7 +151,13 @@ int csemb_plan_destroy(csemb_plan *p);
 #define CSEMB_OPT_EXACT_PEAKS 1
 #define CSEMB_OPT_REVERSE_SWEEP 2
 #define CSEMB_OPT_SPLIT_THRESHOLD 3 /* rows longer than this (default 2048) are split
-                                       into 1024-entry chunks summed in chunk order;
+                                       into chunks of <= 1024 entries summed in chunk
+                                       order; on matrices with >= 8 column windows of
+                                       3*2^16 (f32) / 2^16 (f64) columns the limit is
+                                       min(this, max(64, 20 * windows)) and rows up to
+                                       65536 entries are cut at the window boundaries
+                                       (the cuts depend on the matrix and dtype only,
+                                       never on the block width);
                                        0 = never split (bit-exact for every input) */
 #define CSEMB_OPT_ROW_ORDER 4       /* -1 auto (default: 1 for skewed row lengths,
                                        else 2), 0 natural, 1 bucketed by batch count,

@@ -14,8 +14,11 @@ between the host arrays and the result runs on the GPU through the C ABI
 
 Exactness: fp64 results are bit-identical to the reference for every matrix
 whose rows all have at most `split_threshold` stored entries (default 2048:
-configs 1-2 and every reference test).  Longer rows are summed as 1024-entry
-chunk partials added in chunk order (load balance for power-law rows), which
+configs 1-2 and every reference test; min(2048, max(64, 20 * windows)) on
+matrices with >= 8 column windows of 3*2^16 (f32) / 2^16 (f64) columns, where
+moderately heavy rows are cut at the windows so their gathers stay in L2).
+Longer rows are summed as chunk partials (<= 1024 entries) added in chunk
+order (load balance for power-law rows), which
 changes only those rows' rounding -- measured within 1e-13 relative Frobenius
 on configs 3/4 shapes against the oracle, inside north_star's 1e-10 gate.
 `Plan.set_load_balance(split_threshold=0)` (CSEMB_OPT_SPLIT_THRESHOLD 0)
