@@ -503,6 +503,7 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
     }
     if (wcols >= m->n_cols) wcols = 0;  // one window: plain fixed chunks
     if (threshold <= 0) wcols = 0;
+    const int64_t caller_threshold = threshold;
     if (wcols > 0) {
         const int64_t nw = (m->n_cols + wcols - 1) / wcols;
         threshold = std::min<int64_t>(threshold, std::max<int64_t>(64, nw * 20));
@@ -606,6 +607,39 @@ static int get_schedule_impl(csemb_mat *m, int G, int64_t threshold, int order, 
         if (e != cudaSuccess) {
             cudaGetLastError();
             return fail(CSEMB_ERR_CUDA, "schedule window bounds: %s", cudaGetErrorString(e));
+        }
+    }
+    // A row under the caller's threshold is only worth cutting when its entries are
+    // spread over the columns: one whose entries fall in fewer than 3 windows (a
+    // banded matrix) gathers locally already and goes back to the light rows.
+    if (wcols > 0 && !hrows.empty()) {
+        std::vector<int> keep, demoted;
+        std::vector<int64_t> kb;
+        for (size_t h = 0; h < hrows.size(); ++h) {
+            const int r = hrows[h];
+            const int64_t *bw = bounds.data() + h * (size_t)(nwin + 1);
+            if (rp[r + 1] - rp[r] <= caller_threshold) {
+                int nseg = 0;
+                for (int k = 0; k < nwin && nseg < 3; ++k) nseg += bw[k + 1] > bw[k];
+                if (nseg < 3) {
+                    demoted.push_back(r);
+                    continue;
+                }
+            }
+            keep.push_back(r);
+            kb.insert(kb.end(), bw, bw + nwin + 1);
+        }
+        if (!demoted.empty()) {
+            std::vector<int> merged(light.size() + demoted.size());
+            std::merge(light.begin(), light.end(), demoted.begin(), demoted.end(), merged.begin());
+            light.swap(merged);
+            for (int r : demoted) {
+                const double len = (double)(rp[r + 1] - rp[r]);
+                sum += len;
+                sum2 += len * len;
+            }
+            hrows.swap(keep);
+            bounds.swap(kb);
         }
     }
     // hot heavy rows: rank (by descending length) of heavy row h, or -1

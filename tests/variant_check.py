@@ -81,6 +81,19 @@ def main():
     plan.set_load_balance(split_threshold=64)
     assert rel(plan.apply(th, 1, om), ref) <= 1e-13
     dm.close()
+    # banded matrix, 320 entries per row within +-160 columns: over the windowed split
+    # threshold when CSEMB_HEAVY_WINDOW_MB is tiny, but every row's entries fall in one
+    # or two windows, so the schedule sends them back to the light rows -- strict
+    # stored order, bit-exact in every variant
+    n = 30000
+    base = np.arange(n, dtype=np.int64)
+    e = np.concatenate([np.stack([base, (base + k) % n], 1) for k in range(1, 161)])
+    S = pb.normalized_adjacency(e, n)
+    om = O.sample_projection(n, 16, 9)
+    th = pb.legendre_coefficients(pb.indicator_above(0.5), 4).coeffs
+    ref = oracle_embed(S, th, om)
+    assert np.array_equal(pb.fast_embed_eig(S, pb.LegendreExpansion(th), 4, om).values, ref), "band fp64 differs"
+    assert rel(pb.fast_embed_eig(S, pb.LegendreExpansion(th), 4, om, dtype="float32").values, ref) <= 1e-4
     print("VARIANT_OK")
 
 
