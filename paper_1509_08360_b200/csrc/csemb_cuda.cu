@@ -160,6 +160,14 @@ static cudaError_t run_step_t(const StepParams &P0, cudaStream_t s, int sm_count
     const int W = Vec<T>::W;
     const int nch = ((P0.col0 + (P0.v0 + P0.nvt) * W - 1) >> 5) - ((P0.col0 + P0.v0 * W) >> 5) + 1;
     StepParams P = P0;
+#if K1_HOTCOL
+    {
+        static const int hb = getenv("CSEMB_HOT_COL_BELOW") ? atoi(getenv("CSEMB_HOT_COL_BELOW")) : 0;
+        P.hot_below = hb;
+    }
+#else
+    P.hot_below = 0;
+#endif
     size_t smem = MODE == MODE_RECUR ? (size_t)(nch + 1) * 8 : 0;
     size_t max_smem = 1024;
     if (STAGED) {

@@ -174,6 +174,7 @@ struct StepParams {
     // checked bit for bit on the device by k_vf_check), so K1 recomputes the
     // value from the row offsets instead of streaming it (null: read values)
     const int *vf;
+    int hot_below;  // K1_HOTCOL experiment builds: columns below this allocate in L1, others do not (0: off)
 };
 
 __device__ __forceinline__ bool memcmp_eq(double a, double b) { return __double_as_longlong(a) == __double_as_longlong(b); }
@@ -310,6 +311,18 @@ __device__ __forceinline__ void ld_gather_into(double2 &v, const double2 *p, boo
 }
 __device__ __forceinline__ void ld_gather_into(float4 &v, const float4 *p, bool ok) {
     asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q " GATHER_OP ".v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(p), "r"((unsigned)ok));
+}
+#ifndef K1_HOTCOL
+#define K1_HOTCOL 0  // 1 (experiment build): gathers of columns >= StepParams::hot_below do not allocate in L1
+#endif
+// predicated L1-no-allocate gather into a live register (K1_HOTCOL experiment)
+__device__ __forceinline__ void ld_gather_na_into(double2 &v, const double2 *p, bool ok) {
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];\n}"
+        : "+d"(v.x), "+d"(v.y) : "l"(p), "r"((unsigned)ok));
+}
+__device__ __forceinline__ void ld_gather_na_into(float4 &v, const float4 *p, bool ok) {
+    asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n}"
         : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(p), "r"((unsigned)ok));
 }
 __device__ __forceinline__ double2 vsel(bool c, double2 a, double2 b) {
@@ -608,6 +621,17 @@ __global__ void __launch_bounds__(256, (K1_MIN_BLOCKS ? K1_MIN_BLOCKS : 2)) k_st
             }
         } else {
             const VT *x = ycur + (int64_t)j * P.ldv;
+#if K1_HOTCOL
+            if (P.hot_below > 0) {  // warp-uniform: hot columns allocate in L1, the rest bypass it
+                const bool hot = j < P.hot_below;
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    buf[slot][k] = ld_gather_if(x + k * G, valid[k] && ok && hot);
+                    ld_gather_na_into(buf[slot][k], x + k * G, valid[k] && ok && !hot);
+                }
+                return;
+            }
+#endif
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 if (K1_KEEP_STALE)
