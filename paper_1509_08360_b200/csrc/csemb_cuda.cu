@@ -254,6 +254,11 @@ static cudaError_t dispatch_vpl(int vpl, const StepParams &P, cudaStream_t s, in
             if (vpl == 5) return run_step<T, G, 5, MODE, PEAK>(P, s, sm);
         }
 #endif
+#if !K1_WIDE_VPL
+        if constexpr (G == 8) {  // 33..40 vectors on 8 lanes (choose_group)
+            if (vpl == 5) return run_step<T, G, 5, MODE, PEAK>(P, s, sm);
+        }
+#endif
         switch (vpl) {
             case 2: return run_step<T, G, 2, MODE, PEAK>(P, s, sm);
             case 3: return run_step<T, G, 3, MODE, PEAK>(P, s, sm);
@@ -278,8 +283,24 @@ static int target_vpl() {
     return t;
 }
 
+// Rows of 33..40 vectors (fp64 d = 65..80: config 2) run on 8 lanes x 5 vectors
+// instead of 16 lanes x 3: every lane slot carries data (40 of 40 instead of 40
+// of 48), so a step issues fewer gather and arithmetic instructions for the same
+// bytes.  At full clock that is worth 2% (round 2, session 1); under the
+// sustained 1 kW power cap, where K1's time follows its energy per step, it is
+// worth 6% (session 4: 250.9 -> 235.9 ms per config-2 embedding, K1 1.40 -> 1.31
+// ms).  CSEMB_WIDE_SHAPE=0 restores 16 x 3.
+static bool wide_shape() {
+    static const bool on = [] {
+        const char *e = getenv("CSEMB_WIDE_SHAPE");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 static int choose_group(int nv) {
     const int tv = target_vpl();
+    if (tv == 3 && nv >= 33 && nv <= 40 && wide_shape()) return 8;
     int g = 1;
     while (g < 32 && (nv + g - 1) / g > tv) g *= 2;
     // one lane per row loads 16 bytes of 32 different rows per instruction (32
